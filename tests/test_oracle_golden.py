@@ -1,0 +1,47 @@
+"""Pin the CPU oracle (oracle/hevi_oracle.py) against fixtures produced by
+the unmodified reference (tests/golden/make_golden.py).  CPU only."""
+import numpy as np
+import pytest
+
+from conftest import CASES, load_golden, oracle_for, rel_fields
+
+OPS_TOL = 1e-12      # oracle restates the same numpy arithmetic
+STEP_TOL = 1e-12
+
+
+@pytest.fixture(scope="module", params=sorted(CASES))
+def case(request):
+    return request.param, oracle_for(request.param), load_golden(request.param)
+
+
+def test_oracle_operators_match_reference(case):
+    name, o, g = case
+    q = o.from_lattice(g["ops_q"])
+    for got, want in ((o.rhs(q), g["ops_R"]), (o.linear(q), g["ops_L"]),
+                      (o.solve(q, float(g["ops_lam"])), g["ops_solve"])):
+        errs = rel_fields(o.to_lattice(got), want)
+        assert max(errs) < OPS_TOL, (name, errs)
+
+
+def test_oracle_column_matrix_matches_probed_reference(case):
+    name, o, g = case
+    A, nb = o.column_matrices(float(g["ops_lam"]))
+    assert nb == int(g["col_nb"])
+    assert np.abs(A[0] - g["col_A0"]).max() <= 1e-14 * np.abs(g["col_A0"]).max()
+    # box meshes: every column carries the same matrix (SURVEY finding 5)
+    assert np.abs(A - A[0:1]).max() <= 1e-12 * np.abs(A).max()
+    LU = o.band_lu(A.copy(), nb)
+    assert np.abs(LU[0] - g["col_LU0"]).max() <= 1e-13 * np.abs(g["col_LU0"]).max()
+
+
+def test_oracle_steps_match_reference(case):
+    name, o, g = case
+    q = o.from_lattice(g["step_q0"])
+    dt = float(g["step_dt"])
+    assert abs(o.dt_for_courant(q, CASES[name]["courant"]) - dt) <= 1e-14 * dt
+    keep = sorted(int(k[6:]) for k in g.files if k.startswith("step_q") and k != "step_q0")
+    for k in range(1, keep[-1] + 1):
+        q = o.step(q, dt)
+        if k in keep:
+            errs = rel_fields(o.to_lattice(q), g[f"step_q{k}"])
+            assert max(errs) < STEP_TOL, (name, k, errs)
