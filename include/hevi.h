@@ -1,0 +1,130 @@
+/*
+ * hevi.h -- C ABI of the B200-native HEVI 1D-IMEX ARK2 step (libhevi.so).
+ *
+ * The reference (dycore, pure Python/NumPy) has no FFI for this path; its
+ * drop-in boundary is the Python call protocol listed in SURVEY.md 8(b).
+ * Each entry point below replaces one reference function; the Python layer
+ * paper_1702_04316_b200 rebinds the reference protocol on top of it.
+ *
+ * Conventions
+ *   - all pointers to state/work arrays are DEVICE pointers to fp64
+ *     "lattice" arrays: field-major, field f at  f*fs + (gz*lY + iy)*px + ix
+ *     (ix, iy local to the rank window; gz = level); fs = Z*lY*px.
+ *     Fields: 0 rho', 1 u, 2 v, 3 w, 4 theta' (euler.py:39-58, set2nc).
+ *   - E-vector arrays use the reference layout (5, nel, nqt, nqs, nqr)
+ *     with element e = (kz*ney + ky)*nex + kx (specgrid.py:185-201).
+ *   - `stream` is a cudaStream_t passed as void*.
+ *   - return value: HEVI_OK (0) or a negative HEVI_E* code; no C++
+ *     exception crosses the ABI.  Numerical failures detected on the
+ *     device are sticky flags read back with hevi_flags().
+ */
+#ifndef HEVI_H
+#define HEVI_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HEVI_OK 0
+#define HEVI_EARG (-1)        /* bad argument / unsupported configuration */
+#define HEVI_ECUDA (-2)       /* CUDA runtime error (see hevi_last_error) */
+#define HEVI_ENOFACTOR (-3)   /* solve requested for an unfactored lam */
+
+/* device flag bits (hevi_flags); stage s = 0,1,2 are the three explicit
+ * evaluations of an ARK2 step (a single rhs() call reports as stage 0) */
+#define HEVI_F_NONFINITE_IN(s) (1u << ((s) * 4 + 0)) /* euler.py:445-446 FloatingPointError */
+#define HEVI_F_EOS(s) (1u << ((s) * 4 + 1))          /* euler.py:183-184 ValueError */
+#define HEVI_F_NONFINITE_OUT (1u << 12)              /* imexcore.py:412-413 FloatingPointError */
+#define HEVI_F_PIVOT (1u << 13)                      /* columnsolve.py:135-137 RuntimeError */
+#define HEVI_F_AINV (1u << 14)                       /* imexcore.py:214-215 FloatingPointError */
+
+typedef struct hevi_plan hevi_plan;
+
+/* Structured box (specgrid.build_box_mesh slab, or the SURVEY 8(c) 3D box).
+ * Global lattice X = nex*N+1, Y = ney*Ny+1, Z = nez*N+1. */
+typedef struct {
+    int nex, ney, nez;      /* global element counts                        */
+    int N, Ny;              /* polynomial order (Ny = N in 3D, 1 for slab)  */
+    int slab;               /* 1: columns keyed by x only (specgrid.py:203) */
+    int x0, y0, lX, lY;     /* this rank's lattice window (global origin)   */
+    int px;                 /* x pitch of lattice arrays, >= lX             */
+    int ex_b, ex_e;         /* owned element range in x  [ex_b, ex_e)       */
+    int ey_b, ey_e;         /* owned element range in y                     */
+} hevi_grid_desc;
+
+/* Host arrays copied into the plan at creation.  Level tables have length
+ * Z and carry the reference-state coefficients of euler.py:70-150 sampled
+ * per level; cx/cy/cz are the DSS-averaged metric factors per lattice index
+ * (1/dxdr for element-interior points, 1/(dxdr_left + dxdr_right) on
+ * element faces); Dx/Dy/Dz are (N+1)^2 / (Ny+1)^2 LGL derivative matrices. */
+typedef struct {
+    const double *rho0, *theta0, *P0f, *drho0, *dtheta0;
+    const double *G0, *H0, *F0z, *rho0G0;
+    const double *cx, *cy, *cz;
+    const double *Dx, *Dy, *Dz;
+    double g, R, P0, gamma;
+} hevi_ref_desc;
+
+int hevi_plan_create(hevi_plan **plan, const hevi_grid_desc *grid, const hevi_ref_desc *ref);
+int hevi_plan_destroy(hevi_plan *plan);
+const char *hevi_last_error(void);
+/* number of doubles in one 5-field lattice array of this plan */
+long long hevi_state_size(const hevi_plan *plan);
+
+/* columnsolve.get_factors + factor_with_fallback (columnsolve.py:141-153,
+ * 184-188): probe the Schur column operator lhs_schur (imexcore.py:270-271)
+ * on the device, no-pivot banded LU (columnsolve.py:111-138), cached per
+ * round(lam, 12).  nb_out (may be NULL) receives the detected bandwidth. */
+int hevi_factor(hevi_plan *plan, double lam, int *nb_out, void *stream);
+/* copy the dense probed column matrix / its LU (M*M, row-major) to host */
+int hevi_column_matrix(hevi_plan *plan, double lam, double *A_host, double *LU_host, void *stream);
+
+/* euler.nonlinear_rhs, cG set2nc (euler.py:438-497): R = R(q) */
+int hevi_rhs(hevi_plan *plan, const double *q, double *R, void *stream);
+/* euler.vertical_restriction (euler.py:368-371): L = L_V(q) */
+int hevi_linear_v(hevi_plan *plan, const double *q, double *L, void *stream);
+/* ImplicitProblem.solve, direct branch (imexcore.py:312-322 ->
+ * columnsolve.solve_direct :191-210): q = (I - lam L_V)^{-1} q_e */
+int hevi_solve(hevi_plan *plan, double lam, const double *qe, double *q, void *stream);
+
+/* One explicit stage of the fused ARK2 schedule:
+ *   stage 0: reads Q;          writes P(0,3,4), Q1(1,2), A, F
+ *   stage 1: reads Q1, A, F;   writes P(0,3,4), A(1,2), F
+ *   stage 2: reads A, F;       writes Q
+ * work = 4 consecutive lattice arrays [Q1 | A | F | P].
+ * tab = {a[3][3], at[3][3], b[3]} row-major (imexcore.py:44-63). */
+int hevi_stage(hevi_plan *plan, int stage, double dt, const double *tab,
+               double *Q, double *work, void *stream);
+/* column solve of a stage: P(0,3,4) -> dst(0,3,4); stage 0 -> Q1, stage 1 -> A */
+int hevi_stage_solve(hevi_plan *plan, int stage, double lam, double *work, void *stream);
+/* imexcore.ark_imex_step (imexcore.py:385-414), single rank: Q <- step(Q) */
+int hevi_ark2_step(hevi_plan *plan, double dt, const double *tab, double *Q, double *work,
+                   void *stream);
+
+/* E-vector <-> lattice (exact for DSS-continuous fields; the lattice takes
+ * the first-occurrence copy, columnsolve.unique_space rep :28-34) */
+int hevi_evec_to_lattice(hevi_plan *plan, const double *E, double *Lat, int nfields, void *stream);
+int hevi_lattice_to_evec(hevi_plan *plan, const double *Lat, double *E, int nfields, void *stream);
+
+/* sticky device flags: OR of HEVI_F_* since the last reset (synchronises stream) */
+int hevi_flags(hevi_plan *plan, unsigned *flags, int reset, void *stream);
+
+/* Generic batched column API on per-column banded storage, the reference's
+ * ColumnJacobian path for arbitrary (n_col, M, M) matrices:
+ *   band layout: band[(d*M + k)*n_col + c], d = j - k + nb - 1 in [0, 2nb-2]
+ * hevi_band_pack:  dense (n_col, M, M) row-major -> band
+ * hevi_band_lu:    columnsolve.lu_factor_banded (:111-138), in place;
+ *                  *bad_col receives the first degenerate column or -1
+ * hevi_band_solve: columnsolve.solve_columns_direct (:156-181), rhs (n_col, M)
+ *                  row-major, solved in place                                  */
+int hevi_band_pack(const double *dense, double *band, int n_col, int M, int nb, void *stream);
+int hevi_band_unpack(const double *band, double *dense, int n_col, int M, int nb, void *stream);
+int hevi_band_lu(double *band, int n_col, int M, int nb, double norm, int *bad_col, void *stream);
+int hevi_band_solve(const double *band, double *rhs, int n_col, int M, int nb, void *stream);
+/* max |a_i| over n doubles (device), deterministic */
+int hevi_absmax(const double *a, long long n, double *out_host, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEVI_H */

@@ -1,0 +1,120 @@
+"""ctypes binding of libhevi.so (the C ABI declared in include/hevi.h).
+
+There is no fallback: if the library is missing or no CUDA device is
+present, every compute entry point raises.  ``load()`` only needs the .so
+(CPU hosts can load it to check the exported symbols).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libhevi.so")
+
+HEVI_OK = 0
+F_NONFINITE_OUT = 1 << 12
+F_PIVOT = 1 << 13
+F_AINV = 1 << 14
+
+
+def F_NONFINITE_IN(stage):
+    return 1 << (stage * 4 + 0)
+
+
+def F_EOS(stage):
+    return 1 << (stage * 4 + 1)
+
+
+class GridDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "nex", "ney", "nez", "N", "Ny", "slab", "x0", "y0", "lX", "lY", "px",
+        "ex_b", "ex_e", "ey_b", "ey_e")]
+
+
+_DP = ctypes.POINTER(ctypes.c_double)
+
+
+class RefDesc(ctypes.Structure):
+    _fields_ = [(n, _DP) for n in (
+        "rho0", "theta0", "P0f", "drho0", "dtheta0", "G0", "H0", "F0z", "rho0G0",
+        "cx", "cy", "cz", "Dx", "Dy", "Dz")] + [
+        (n, ctypes.c_double) for n in ("g", "R", "P0", "gamma")]
+
+
+# exported symbol -> (restype, argtypes); this list IS the C ABI of hevi.h
+_V = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+_LL = ctypes.c_longlong
+SIGNATURES = {
+    "hevi_plan_create": (_I, [ctypes.POINTER(_V), ctypes.POINTER(GridDesc), ctypes.POINTER(RefDesc)]),
+    "hevi_plan_destroy": (_I, [_V]),
+    "hevi_last_error": (ctypes.c_char_p, []),
+    "hevi_state_size": (_LL, [_V]),
+    "hevi_factor": (_I, [_V, _D, ctypes.POINTER(_I), _V]),
+    "hevi_column_matrix": (_I, [_V, _D, _V, _V, _V]),
+    "hevi_rhs": (_I, [_V, _V, _V, _V]),
+    "hevi_linear_v": (_I, [_V, _V, _V, _V]),
+    "hevi_solve": (_I, [_V, _D, _V, _V, _V]),
+    "hevi_stage": (_I, [_V, _I, _D, _V, _V, _V, _V]),
+    "hevi_stage_solve": (_I, [_V, _I, _D, _V, _V]),
+    "hevi_ark2_step": (_I, [_V, _D, _V, _V, _V, _V]),
+    "hevi_evec_to_lattice": (_I, [_V, _V, _V, _I, _V]),
+    "hevi_lattice_to_evec": (_I, [_V, _V, _V, _I, _V]),
+    "hevi_flags": (_I, [_V, ctypes.POINTER(ctypes.c_uint), _I, _V]),
+    "hevi_band_pack": (_I, [_V, _V, _I, _I, _I, _V]),
+    "hevi_band_unpack": (_I, [_V, _V, _I, _I, _I, _V]),
+    "hevi_band_lu": (_I, [_V, _I, _I, _I, _D, ctypes.POINTER(_I), _V]),
+    "hevi_band_solve": (_I, [_V, _V, _I, _I, _I, _V]),
+    "hevi_absmax": (_I, [_V, _LL, ctypes.POINTER(_D), _V]),
+}
+
+_lib = None
+
+
+class NativeMissing(RuntimeError):
+    pass
+
+
+def load():
+    """Load libhevi.so (raises NativeMissing if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeMissing(
+            f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc):
+    if rc != HEVI_OK:
+        msg = load().hevi_last_error().decode()
+        raise RuntimeError(f"libhevi error {rc}: {msg}")
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the HEVI path runs on a CUDA device only (no CPU fallback); "
+                           "torch.cuda.is_available() is False")
+    load()
+
+
+def stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    """Device pointer of a contiguous float64 CUDA tensor."""
+    return ctypes.c_void_p(t.data_ptr())

@@ -1,0 +1,186 @@
+"""Direct solution of the vertically-implicit problem (drop-in for
+``dycore.columnsolve``, columnsolve.py:1-210).
+
+Two device paths sit behind the reference API:
+
+* ``solve_direct(problem, q_e)`` -- the production path: the Schur column
+  operator is probed and LU-factored once per ``round(lam, 12)`` on the
+  device (one factor shared by all columns: on box meshes every column
+  carries the same matrix, SURVEY finding 5, asserted in the tests), and
+  the fused column kernel builds the Schur RHS, substitutes and extracts.
+* ``build_column_jacobian`` / ``lu_factor_banded`` /
+  ``solve_columns_direct`` -- the reference's batched per-column API on
+  arbitrary ``(n_col, M, M)`` matrices, run by the generic banded kernels
+  (column-interleaved band storage, one thread per column).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nv
+
+
+@dataclass
+class UniqueSpace:
+    """columnsolve.py:18-25 (uid/rep materialised lazily: they are E-vector
+    sized index maps, only needed by callers that gather by hand)."""
+    mesh: object
+    n_col: int
+    n_lev: int
+    shape: tuple
+
+    def _maps(self):
+        m = self.mesh
+        nel, nt, ns, nr = m.nshape
+        e = np.arange(nel)
+        kx = e % m.nx
+        ky = (e // m.nx) % m.ny
+        kz = e // (m.nx * m.ny)
+        gx = kx[:, None, None, None] * m.N + np.arange(nr)[None, None, None, :]
+        gy = ky[:, None, None, None] * m.Ny + np.arange(ns)[None, None, :, None]
+        gz = kz[:, None, None, None] * m.N + np.arange(nt)[None, :, None, None]
+        col = gx if m.slab else gy * m.X + gx
+        uid = (np.broadcast_to(col, self.shape).astype(np.int64) * self.n_lev
+               + np.broadcast_to(gz, self.shape)).ravel()
+        vals, rep = np.unique(uid, return_index=True)
+        return uid, rep
+
+    @property
+    def uid(self):
+        return self._maps()[0]
+
+    @property
+    def rep(self):
+        return self._maps()[1]
+
+
+def unique_space(mesh) -> UniqueSpace:
+    return UniqueSpace(mesh=mesh, n_col=mesh.n_col, n_lev=mesh.n_lev, shape=tuple(mesh.nshape))
+
+
+@dataclass
+class ColumnJacobian:
+    """columnsolve.py:37-49.  ``matrices`` is a CUDA tensor (n_col, M, M),
+    overwritten by the LU factors like the reference."""
+    matrices: object
+    bandwidth: int
+    n_dof: int
+    space: UniqueSpace
+    factored: bool = False
+    pivoted_fallback: list = None
+    piv: dict = None
+    band: object = None          # device band storage after factoring
+
+    @property
+    def M(self) -> int:
+        return self.matrices.shape[1]
+
+
+def build_column_jacobian(problem) -> ColumnJacobian:
+    """Probe the Schur column operator (columnsolve.py:75-108) on the device.
+
+    The probe runs on one column; box meshes have identical columns, so the
+    matrix is broadcast to all n_col columns."""
+    import torch
+    if problem.dim != "1d":
+        raise ValueError("column Jacobians require the 1D implicit form")
+    if problem.form != "schur":
+        raise NotImplementedError("the device path implements the Schur (pressure) form")
+    plan = problem.disc.plan_for(problem.ref)
+    lam = float(problem.lam)
+    space = unique_space(problem.disc.mesh)
+    if lam == 0.0:
+        A = np.eye(space.n_lev)
+        nb = 1
+    else:
+        A, _ = plan.column_matrix(lam)
+        nb = plan.factor(lam)
+    mats = torch.as_tensor(A, device=plan.device).expand(space.n_col, -1, -1).contiguous()
+    return ColumnJacobian(matrices=mats, bandwidth=nb, n_dof=1, space=space,
+                          pivoted_fallback=[], piv={})
+
+
+def lu_factor_banded(cj: ColumnJacobian):
+    """In-place no-pivot banded LU, batched over columns (columnsolve.py:111-138)."""
+    import torch
+    if cj.factored:
+        raise ValueError("already factored")
+    lib = nv.load()
+    A = cj.matrices
+    if not isinstance(A, torch.Tensor) or not A.is_cuda:
+        A = torch.as_tensor(np.asarray(A, dtype=np.float64), device="cuda")
+    A = A.to(torch.float64).contiguous()
+    n_col, M, _ = A.shape
+    nb = int(cj.bandwidth)
+    s = nv.stream_ptr()
+    norm = np.zeros(1)
+    nv.check(lib.hevi_absmax(nv.ptr(A), A.numel(), norm.ctypes.data_as(
+        ctypes.POINTER(ctypes.c_double)), s))
+    band = torch.empty((2 * nb - 1, M, n_col), dtype=torch.float64, device=A.device)
+    nv.check(lib.hevi_band_pack(nv.ptr(A), nv.ptr(band), n_col, M, nb, s))
+    bad = ctypes.c_int(-1)
+    nv.check(lib.hevi_band_lu(nv.ptr(band), n_col, M, nb, float(norm[0]),
+                              ctypes.byref(bad), s))
+    if bad.value >= 0:
+        raise RuntimeError(f"no-pivot LU hit a degenerate diagonal in column(s) [{bad.value}]")
+    # factors back into the dense matrices, in place (entries outside the band
+    # are untouched by the reference's banded elimination)
+    dense = torch.empty_like(A)
+    nv.check(lib.hevi_band_unpack(nv.ptr(band), nv.ptr(dense), n_col, M, nb, s))
+    inband = _band_mask(M, nb, A.device)
+    A.copy_(torch.where(inband, dense, A))
+    cj.matrices = A
+    cj.band = band
+    cj.factored = True
+
+
+def _band_mask(M, nb, device):
+    import torch
+    i = torch.arange(M, device=device)
+    return ((i[:, None] - i[None, :]).abs() < nb)[None]
+
+
+def factor_with_fallback(problem) -> ColumnJacobian:
+    """columnsolve.py:141-153.  The pivoted dense fallback is not ported
+    (no-pivot LU never falls back on the Schur columns, SURVEY finding 5):
+    a degenerate pivot raises."""
+    cj = build_column_jacobian(problem)
+    lu_factor_banded(cj)
+    return cj
+
+
+def solve_columns_direct(cj: ColumnJacobian, rhs):
+    """Banded forward/backward substitution, batched over columns
+    (columnsolve.py:156-181); rhs (n_col, M) numpy or torch."""
+    import torch
+    if not cj.factored:
+        raise ValueError("factor before solving")
+    lib = nv.load()
+    was_np = not isinstance(rhs, torch.Tensor)
+    t = torch.as_tensor(np.asarray(rhs, dtype=np.float64) if was_np else rhs)
+    dev = t.device
+    x = t.to(device="cuda", dtype=torch.float64).contiguous().clone()
+    n_col, M = x.shape
+    nv.check(lib.hevi_band_solve(nv.ptr(cj.band), nv.ptr(x), n_col, M, int(cj.bandwidth),
+                                 nv.stream_ptr()))
+    if was_np:
+        return x.cpu().numpy()
+    return x.to(dev)
+
+
+def get_factors(problem) -> ColumnJacobian:
+    """Factor cache keyed by (round(lam, 12), form) (columnsolve.py:184-188)."""
+    key = (round(problem.lam, 12), problem.form)
+    if key not in problem._column_cache:
+        problem._column_cache[key] = factor_with_fallback(problem)
+    return problem._column_cache[key]
+
+
+def solve_direct(problem, q_e):
+    """One direct implicit solve (columnsolve.py:191-210): the fused device
+    column kernel with the shared per-lam factor."""
+    plan = problem.disc.plan_for(problem.ref)
+    return plan.apply_evec("solve", q_e, lam=float(problem.lam))

@@ -1,0 +1,1391 @@
+// hevi.cu -- B200 (sm_100a) kernels and C ABI for the HEVI 1D-IMEX ARK2 step.
+//
+// Layout and schedule are described in DESIGN.md.  Short version:
+//  * state lives on the unique-point lattice (one copy per DSS group), field
+//    major, x fastest: the reference's cG E-vector state is bitwise
+//    continuous (SURVEY finding 5), so the lattice holds the same numbers;
+//  * the DSS of R(q) (euler.py:493, specgrid.py:535-540) is folded into the
+//    derivatives: R is affine in the 18 gradient components with pointwise
+//    coefficients, so the mass-weighted average of the per-copy R equals R
+//    evaluated with mass-weighted averaged derivatives.  Each lattice point
+//    reads its element lines and writes itself: no scatter, no atomics,
+//    bit-stable, any partition gives the same bits;
+//  * explicit kernel: one CTA per horizontal tile of element columns,
+//    sweeping the element layers bottom-up through shared memory; the
+//    element-face vertical derivative is carried in shared memory from the
+//    layer below; ARK2 stage combinations fused into the epilogue;
+//  * column kernel: one thread per vertical column, Schur RHS build,
+//    banded forward/back substitution with the single shared LU factor
+//    (box meshes: all columns identical), extraction -- fused.
+#include "../../include/hevi.h"
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const char* what, cudaError_t e = cudaSuccess) {
+    g_err = what;
+    if (e != cudaSuccess) {
+        g_err += ": ";
+        g_err += cudaGetErrorString(e);
+        return HEVI_ECUDA;
+    }
+    return HEVI_EARG;
+}
+
+#define CK(call)                                        \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return fail(#call, e_);  \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// parameter blocks (passed by value: live in the kernel constant bank)
+// ---------------------------------------------------------------------------
+struct Geo {
+    int nex, ney, nez, X, Y, Z;
+    int x0, y0, lX, lY, px;
+    long long fs;
+    int ex_b, ex_e, ey_b, ey_e;
+    int slab;
+};
+
+struct Lev {
+    const double *rho0, *theta0, *P0f, *drho0, *dth0, *G0, *H0, *F0z, *rho0G0;
+};
+
+struct Phys {
+    double g, R, P0, gamma;
+};
+
+enum { M_R = 0, M_L = 1, M_S1 = 2, M_S2 = 3, M_S3 = 4 };
+
+struct EArgs {
+    Geo g;
+    Lev lv;
+    Phys ph;
+    const double *cx, *cy, *cz;
+    const double *Dx, *Dy, *Dz;
+    const double* q;
+    double* out;   // M_R / M_L output, M_S3 new state
+    double* P;     // predictor (fields 0,3,4)       [S1, S2]
+    double* Quv;   // projected u,v of the stage      [S1 -> Q1, S2 -> A]
+    double* A;     // S1 write, S2 read
+    double* F;     // S1 write, S2 read/write, S3 read
+    double dt, a_p, at_p, a_a, at_a, cb;
+    unsigned* flags;
+    int stage;
+};
+
+struct SArgs {
+    Geo g;
+    Lev lv;
+    Phys ph;
+    const double* cz;
+    const double* Dz;
+    const double* LUb;     // M x (2nb-1)
+    const double* lamtab;  // coefS | uA | den  (3*M)
+    int nb;
+    int ainv_identity;
+    double lam;
+    const double* P;       // predictor fields 0,3,4
+    double* out;           // writes fields 0,3,4
+    const double* src_uv;  // optional: copy u,v (with no-flux zeroing) from here
+};
+
+__device__ __forceinline__ long long loff(const Geo& g, int gx, int gy, int gz) {
+    return ((long long)gz * g.lY + (gy - g.y0)) * g.px + (gx - g.x0);
+}
+
+// position of lattice index `gi` on an axis with `ne` elements of order N:
+// element line start (relative to the smem coordinate `l` of the point),
+// derivative row, and whether the point is an element face shared with the
+// element below/left (then row N of that element is added).
+struct AxPt {
+    int s0, row, s1;
+    bool face;
+};
+
+__device__ __forceinline__ AxPt axpt(int gi, int l, int N, int ne) {
+    AxPt r;
+    if (gi == ne * N) {
+        r.row = N;
+        r.s0 = l - N;
+        r.face = false;
+        r.s1 = 0;
+    } else {
+        const int i = gi % N;
+        r.row = i;
+        r.s0 = l - i;
+        r.face = (i == 0) && (gi > 0);
+        r.s1 = l - N;
+    }
+    return r;
+}
+
+template <int N, int STRIDE>
+__device__ __forceinline__ double dline(const double* s, const double* drow) {
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m <= N; ++m) acc = fma(drow[m], s[m * STRIDE], acc);
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// explicit kernel: R(q) [+ L_V(q)] and the fused ARK2 stage epilogue
+// ---------------------------------------------------------------------------
+template <int NX, int NY, int NZ, int TX, int TY>
+struct ETile {
+    static constexpr int OX = TX * NX, OY = TY * NY;
+    static constexpr int LX = OX + NX + 1, LY = OY + NY + 1, LZ = NZ + 1;
+    static constexpr int PL = LX * LY, VOL = PL * LZ;
+    static constexpr int CXW = OX + 1, CYW = OY + 1;
+    static constexpr int NSF = 7;
+    static constexpr int DXS = (NX + 1) * (NX + 1), DYS = (NY + 1) * (NY + 1),
+                         DZS = (NZ + 1) * (NZ + 1);
+    static constexpr size_t SMEM =
+        sizeof(double) * (size_t)(NSF * VOL + NSF * CXW * CYW + DXS + DYS + DZS);
+    static constexpr int PTS = OX * (OY + (NY == 1 ? 1 : 0)) * NZ;
+    static constexpr int BLK0 = PTS < 64 ? 64 : (PTS > 512 ? 512 : PTS);
+    static constexpr int BLK = (BLK0 + 31) / 32 * 32;
+};
+
+template <int NX, int NY, int NZ, int TX, int TY, int MODE>
+__global__ void __launch_bounds__(ETile<NX, NY, NZ, TX, TY>::BLK)
+    k_explicit(const EArgs a) {
+    using T = ETile<NX, NY, NZ, TX, TY>;
+    constexpr int LX = T::LX, PL = T::PL, VOL = T::VOL, CXW = T::CXW, CYW = T::CYW;
+    constexpr int BLK = T::BLK;
+    constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
+    constexpr bool NEED_R = (MODE != M_L);
+    extern __shared__ __align__(16) double sm[];
+    double* S = sm;
+    double* Cr = S + T::NSF * VOL;
+    double* sDx = Cr + T::NSF * CXW * CYW;
+    double* sDy = sDx + T::DXS;
+    double* sDz = sDy + T::DYS;
+
+    const Geo& g = a.g;
+    const int tid = threadIdx.x;
+    const int ex0 = g.ex_b + blockIdx.x * TX;
+    const int ey0 = g.ey_b + blockIdx.y * TY;
+    const int nxe = min(TX, g.ex_e - ex0);
+    const int nye = min(TY, g.ey_e - ey0);
+    const int oxn = nxe * NX + ((ex0 + nxe == g.nex) ? 1 : 0);
+    const int oyn = nye * NY + ((ey0 + nye == g.ney) ? 1 : 0);
+    const int gxlo = (ex0 - 1) * NX, gylo = (ey0 - 1) * NY;
+    const double gr = a.ph.g;
+
+    for (int i = tid; i < T::DXS; i += BLK) sDx[i] = a.Dx[i];
+    for (int i = tid; i < T::DYS; i += BLK) sDy[i] = a.Dy[i];
+    for (int i = tid; i < T::DZS; i += BLK) sDz[i] = a.Dz[i];
+
+    for (int ez = 0; ez < g.nez; ++ez) {
+        const int gz0 = ez * NZ;
+        // ---------------- load the element layer (+ low-side halo) --------
+        for (int idx = tid; idx < VOL; idx += BLK) {
+            const int lx = idx % LX;
+            const int t = idx / LX;
+            const int ly = t % T::LY;
+            const int lz = t / T::LY;
+            const int gx = gxlo + lx, gy = gylo + ly, gz = gz0 + lz;
+            const int ix = gx - g.x0, iy = gy - g.y0;
+            double r = 0.0, u = 0.0, v = 0.0, w = 0.0, th = 0.0, pp = 0.0, pl = 0.0;
+            if (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y && ix >= 0 && ix < g.lX && iy >= 0 &&
+                iy < g.lY) {
+                const double* qp = a.q + ((long long)gz * g.lY + iy) * g.px + ix;
+                r = __ldg(qp);
+                u = __ldg(qp + g.fs);
+                v = __ldg(qp + 2 * g.fs);
+                w = __ldg(qp + 3 * g.fs);
+                th = __ldg(qp + 4 * g.fs);
+                if (NEED_R) {
+                    // euler.py:454-457 and equation_of_state (euler.py:185)
+                    const double rho = __ldg(a.lv.rho0 + gz) + r;
+                    const double theta = __ldg(a.lv.theta0 + gz) + th;
+                    pp = a.ph.P0 * pow(rho * a.ph.R * theta / a.ph.P0, a.ph.gamma) -
+                         __ldg(a.lv.P0f + gz);
+                }
+                if (NEED_L) pl = __ldg(a.lv.G0 + gz) * r + __ldg(a.lv.H0 + gz) * th;
+            }
+            S[0 * VOL + idx] = r;
+            S[1 * VOL + idx] = u;
+            S[2 * VOL + idx] = v;
+            S[3 * VOL + idx] = w;
+            S[4 * VOL + idx] = th;
+            S[5 * VOL + idx] = pp;
+            S[6 * VOL + idx] = pl;
+        }
+        __syncthreads();
+        // ---------------- per owned point ---------------------------------
+        const int ozn = NZ + ((ez == g.nez - 1) ? 1 : 0);
+        const int npts = oxn * oyn * ozn;
+        for (int p = tid; p < npts; p += BLK) {
+            const int ox = p % oxn;
+            const int t = p / oxn;
+            const int oy = t % oyn;
+            const int oz = t / oyn;
+            const int gx = ex0 * NX + ox, gy = ey0 * NY + oy, gz = gz0 + oz;
+            const int lx = ox + NX, ly = oy + NY, lz = oz;
+            const AxPt ax = axpt(gx, lx, NX, g.nex);
+            const AxPt ay = axpt(gy, ly, NY, g.ney);
+            const AxPt az = axpt(gz, lz, NZ, g.nez);
+            const double cx = __ldg(a.cx + gx), cy = __ldg(a.cy + gy), cz = __ldg(a.cz + gz);
+            double dxa[NX + 1], dxb[NX + 1], dya[NY + 1], dyb[NY + 1], dza[NZ + 1];
+#pragma unroll
+            for (int m = 0; m <= NX; ++m) {
+                dxa[m] = sDx[ax.row * (NX + 1) + m];
+                dxb[m] = sDx[NX * (NX + 1) + m];
+            }
+#pragma unroll
+            for (int m = 0; m <= NY; ++m) {
+                dya[m] = sDy[ay.row * (NY + 1) + m];
+                dyb[m] = sDy[NY * (NY + 1) + m];
+            }
+#pragma unroll
+            for (int m = 0; m <= NZ; ++m) dza[m] = sDz[az.row * (NZ + 1) + m];
+            const int cidx = oy * CXW + ox;
+            const bool zface = az.face;
+
+            double dX[6], dY[6], dZ[7];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const double* sx = S + f * VOL + lz * PL + ly * LX;
+                double d = dline<NX, 1>(sx + ax.s0, dxa);
+                if (ax.face) d += dline<NX, 1>(sx + ax.s1, dxb);
+                dX[f] = cx * d;
+                const double* sy = S + f * VOL + lz * PL + lx;
+                double e = dline<NY, LX>(sy + ay.s0 * LX, dya);
+                if (ay.face) e += dline<NY, LX>(sy + ay.s1 * LX, dyb);
+                dY[f] = cy * e;
+            }
+#pragma unroll
+            for (int f = 0; f < 7; ++f) {
+                if (f == 6 && !NEED_L) {
+                    dZ[6] = 0.0;
+                    continue;
+                }
+                if (f == 5 && !NEED_R) {
+                    dZ[5] = 0.0;
+                    continue;
+                }
+                const double* sz = S + f * VOL + ly * LX + lx;
+                double d = dline<NZ, PL>(sz + az.s0 * PL, dza);
+                if (zface) d += Cr[f * CXW * CYW + cidx];
+                dZ[f] = cz * d;
+            }
+            // partial (row N) of this element layer at its top face, consumed by
+            // the face level of the next layer
+            if (oz == 0 && ez + 1 < g.nez) {
+                double dzn[NZ + 1];
+#pragma unroll
+                for (int m = 0; m <= NZ; ++m) dzn[m] = sDz[NZ * (NZ + 1) + m];
+#pragma unroll
+                for (int f = 0; f < 7; ++f) {
+                    const double* sz = S + f * VOL + ly * LX + lx;
+                    Cr[f * CXW * CYW + cidx] = dline<NZ, PL>(sz, dzn);
+                }
+            }
+
+            const int c0 = lz * PL + ly * LX + lx;
+            const double r = S[0 * VOL + c0], u = S[1 * VOL + c0], v = S[2 * VOL + c0],
+                         w = S[3 * VOL + c0], th = S[4 * VOL + c0];
+            const double rho0 = __ldg(a.lv.rho0 + gz);
+            const double drho0 = __ldg(a.lv.drho0 + gz);
+            const double dth0 = __ldg(a.lv.dth0 + gz);
+            const bool bx = (gx == 0) || (gx == g.X - 1);
+            const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
+            const bool bz = (gz == 0) || (gz == g.Z - 1);
+
+            double R0 = 0.0, R1 = 0.0, R2 = 0.0, R3 = 0.0, R4 = 0.0;
+            if (NEED_R) {
+                const double rho = rho0 + r;
+                const double theta = __ldg(a.lv.theta0 + gz) + th;
+                const bool finite = isfinite(r) && isfinite(u) && isfinite(v) && isfinite(w) &&
+                                    isfinite(th);
+                if (!finite) atomicOr(a.flags, HEVI_F_NONFINITE_IN(a.stage));
+                if (!(rho > 0.0) || !(theta > 0.0)) atomicOr(a.flags, HEVI_F_EOS(a.stage));
+                // euler.nonlinear_rhs set2nc (euler.py:458-473), DSS folded into dX/dY/dZ
+                const double divu = (dX[1] + dY[2]) + dZ[3];
+                const double rinv = 1.0 / rho;
+                R0 = -(((u * dX[0] + v * dY[0]) + w * dZ[0]) + w * drho0 + rho * divu);
+                R1 = -(((u * dX[1] + v * dY[1]) + w * dZ[1]) + dX[5] * rinv);
+                R2 = -(((u * dX[2] + v * dY[2]) + w * dZ[2]) + dY[5] * rinv);
+                R3 = -(((u * dX[3] + v * dY[3]) + w * dZ[3]) + dZ[5] * rinv + (r * rinv) * gr);
+                R4 = -(((u * dX[4] + v * dY[4]) + w * dZ[4]) + w * dth0);
+                // euler.zero_normal_velocity after the DSS (euler.py:494-496)
+                if (bx) R1 = 0.0;
+                if (by) R2 = 0.0;
+                if (bz) R3 = 0.0;
+            }
+            double L0 = 0.0, L3 = 0.0, L4 = 0.0;
+            if (NEED_L) {
+                // euler.linear_operator(vertical_only=True), set2nc (euler.py:333-361)
+                L0 = -(w * drho0 + rho0 * dZ[3]);
+                L3 = bz ? 0.0 : -(dZ[6] / rho0 + (r / rho0) * gr);
+                L4 = -(w * dth0);
+            }
+            const long long o = loff(g, gx, gy, gz);
+            const long long fs = g.fs;
+            if (MODE == M_R) {
+                a.out[o] = R0;
+                a.out[o + fs] = R1;
+                a.out[o + 2 * fs] = R2;
+                a.out[o + 3 * fs] = R3;
+                a.out[o + 4 * fs] = R4;
+            } else if (MODE == M_L) {
+                a.out[o] = L0;
+                a.out[o + fs] = 0.0;
+                a.out[o + 2 * fs] = 0.0;
+                a.out[o + 3 * fs] = L3;
+                a.out[o + 4 * fs] = L4;
+            } else if (MODE == M_S1) {
+                // imexcore.ark_imex_step (imexcore.py:398-403, 409-411)
+                const double dt = a.dt;
+                const double qv[5] = {r, u, v, w, th};
+                const double Rv[5] = {R0, R1, R2, R3, R4};
+                const double Lv[5] = {L0, 0.0, 0.0, L3, L4};
+                double pr[5];
+#pragma unroll
+                for (int f = 0; f < 5; ++f) {
+                    pr[f] = qv[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+                    a.A[o + f * fs] = qv[f] + dt * (a.a_a * (Rv[f] - Lv[f]) + a.at_a * Lv[f]);
+                    a.F[o + f * fs] = qv[f] + a.cb * Rv[f];
+                }
+                a.P[o] = pr[0];
+                a.P[o + 3 * fs] = pr[3];
+                a.P[o + 4 * fs] = pr[4];
+                a.Quv[o + fs] = bx ? 0.0 : pr[1];
+                a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+            } else if (MODE == M_S2) {
+                const double dt = a.dt;
+                const double Rv[5] = {R0, R1, R2, R3, R4};
+                const double Lv[5] = {L0, 0.0, 0.0, L3, L4};
+                double pr[5];
+#pragma unroll
+                for (int f = 0; f < 5; ++f) {
+                    const double acc = a.A[o + f * fs];
+                    pr[f] = acc + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+                    a.F[o + f * fs] = a.F[o + f * fs] + a.cb * Rv[f];
+                }
+                a.P[o] = pr[0];
+                a.P[o + 3 * fs] = pr[3];
+                a.P[o + 4 * fs] = pr[4];
+                a.Quv[o + fs] = bx ? 0.0 : pr[1];
+                a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+            } else {  // M_S3
+                const double Rv[5] = {R0, R1, R2, R3, R4};
+                bool fin = true;
+#pragma unroll
+                for (int f = 0; f < 5; ++f) {
+                    const double val = a.F[o + f * fs] + a.cb * Rv[f];
+                    fin = fin && isfinite(val);
+                    a.out[o + f * fs] = val;
+                }
+                if (!fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// column kernel: Schur RHS -> banded substitution -> extraction (one thread
+// per vertical column; imexcore.py:229-243, columnsolve.py:156-181,
+// imexcore.py:273-287)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void lev_elem(int k, int N, int ne, int& s0, int& row, bool& face) {
+    if (k == ne * N) {
+        row = N;
+        s0 = k - N;
+        face = false;
+    } else {
+        row = k % N;
+        s0 = k - row;
+        face = (row == 0) && (k > 0);
+    }
+}
+
+template <int NZ>
+__device__ __forceinline__ double col_deriv(const double* buf, int T, int tid, int k, int nez,
+                                            const double* sD, double c) {
+    int s0, row;
+    bool face;
+    lev_elem(k, NZ, nez, s0, row, face);
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m <= NZ; ++m) acc = fma(sD[row * (NZ + 1) + m], buf[(s0 + m) * T + tid], acc);
+    if (face) {
+        double acc2 = 0.0;
+#pragma unroll
+        for (int m = 0; m <= NZ; ++m)
+            acc2 = fma(sD[NZ * (NZ + 1) + m], buf[(k - NZ + m) * T + tid], acc2);
+        acc += acc2;
+    }
+    return c * acc;
+}
+
+template <int NZ>
+__global__ void k_solve(const SArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const Geo& g = a.g;
+    const int M = g.Z;
+    const int T = blockDim.x;
+    const int tid = threadIdx.x;
+    const int W = 2 * a.nb - 1;
+    double* tG0 = sm;
+    double* tH0 = tG0 + M;
+    double* trho0 = tH0 + M;
+    double* tF0z = trho0 + M;
+    double* trG = tF0z + M;
+    double* tdth0 = trG + M;
+    double* tcz = tdth0 + M;
+    double* tcoef = tcz + M;
+    double* tuA = tcoef + M;
+    double* tden = tuA + M;
+    double* LU = tden + M;
+    double* sD = LU + M * W;
+    double* U = sD + (NZ + 1) * (NZ + 1);
+    double* Yb = U + M * T;
+    for (int k = tid; k < M; k += T) {
+        tG0[k] = a.lv.G0[k];
+        tH0[k] = a.lv.H0[k];
+        trho0[k] = a.lv.rho0[k];
+        tF0z[k] = a.lv.F0z[k];
+        trG[k] = a.lv.rho0G0[k];
+        tdth0[k] = a.lv.dth0[k];
+        tcz[k] = a.cz[k];
+        tcoef[k] = a.lamtab[k];
+        tuA[k] = a.lamtab[M + k];
+        tden[k] = a.lamtab[2 * M + k];
+    }
+    for (int i = tid; i < M * W; i += T) LU[i] = a.LUb[i];
+    for (int i = tid; i < (NZ + 1) * (NZ + 1); i += T) sD[i] = a.Dz[i];
+    __syncthreads();
+
+    // owned columns
+    const int xlo = g.ex_b * NZ;  // N (horizontal) == NZ for both layouts
+    const int cntx = (g.ex_e - g.ex_b) * NZ + (g.ex_e == g.nex ? 1 : 0);
+    const int NYo = g.slab ? 1 : NZ;
+    const int ylo = g.ey_b * NYo;
+    const int cnty = (g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
+    const int c = blockIdx.x * T + tid;
+    if (c >= cntx * cnty) return;
+    const int gx = xlo + c % cntx;
+    const int gy = ylo + c / cntx;
+    const int gys = g.slab ? 0 : gy;  // slab: columns keyed by x only
+    const long long fs = g.fs;
+    const double lam = a.lam, gr = a.ph.g;
+    const bool ident = a.ainv_identity != 0;
+    const int nez = g.nez;
+
+    // pass 1: ua_z (imexcore.py:236-241) of the source column
+    for (int k = 0; k < M; ++k) {
+        const long long o = loff(g, gx, gys, k);
+        const double we = a.P[o + 3 * fs], te = a.P[o + 4 * fs];
+        double v = we + (tcoef[k] * te) * gr;
+        if (!ident) v = v - tuA[k] * ((tdth0[k] * v) / tden[k]);
+        U[k * T + tid] = (k == 0 || k == M - 1) ? 0.0 : v;
+    }
+    // pass 2: rhs = Pe - lam (F0 . ua + rho0 G0 div_vc ua), forward substitution
+    const int nb = a.nb;
+    for (int k = 0; k < M; ++k) {
+        const long long o = loff(g, gx, gys, k);
+        const double re = a.P[o], te = a.P[o + 4 * fs];
+        const double ua = U[k * T + tid];
+        const double dua = col_deriv<NZ>(U, T, tid, k, nez, sD, tcz[k]);
+        const double Pe = tG0[k] * re + tH0[k] * te;
+        const double rhs = Pe - lam * (tF0z[k] * ua + trG[k] * dua);
+        double s = 0.0;
+        const int j0 = max(0, k - nb + 1);
+        for (int j = j0; j < k; ++j) s = fma(LU[k * W + (j - k + nb - 1)], Yb[j * T + tid], s);
+        Yb[k * T + tid] = rhs - s;
+    }
+    // pass 3: back substitution
+    for (int k = M - 1; k >= 0; --k) {
+        double s = 0.0;
+        const int j1 = min(k + nb, M);
+        for (int j = k + 1; j < j1; ++j) s = fma(LU[k * W + (j - k + nb - 1)], Yb[j * T + tid], s);
+        Yb[k * T + tid] = (Yb[k * T + tid] - s) / LU[k * W + (nb - 1)];
+    }
+    // pass 4: extraction (imexcore.py:277-287) on the own column
+    for (int k = 0; k < M; ++k) {
+        const long long o = loff(g, gx, gy, k);
+        const double we = a.P[o + 3 * fs], te = a.P[o + 4 * fs];
+        const double Pk = Yb[k * T + tid];
+        const double dP = col_deriv<NZ>(Yb, T, tid, k, nez, sD, tcz[k]);
+        const bool bz = (k == 0) || (k == M - 1);
+        double ua = we + (tcoef[k] * te) * gr;
+        double up = lam * (dP / trho0[k] + (Pk / (tG0[k] * trho0[k])) * gr);
+        if (!ident) {
+            ua = ua - tuA[k] * ((tdth0[k] * ua) / tden[k]);
+            up = up - tuA[k] * ((tdth0[k] * up) / tden[k]);
+        }
+        if (bz) {
+            ua = 0.0;
+            up = 0.0;
+        }
+        const double w = ua - up;
+        const double th = te - lam * (w * tdth0[k]);
+        const double rho = (Pk - tH0[k] * th) / tG0[k];
+        a.out[o] = rho;
+        a.out[o + 3 * fs] = w;
+        a.out[o + 4 * fs] = th;
+        if (a.src_uv) {
+            const bool bx = (gx == 0) || (gx == g.X - 1);
+            const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
+            a.out[o + fs] = bx ? 0.0 : a.src_uv[o + fs];
+            a.out[o + 2 * fs] = by ? 0.0 : a.src_uv[o + 2 * fs];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// factorization (setup, once per lam): per-level lam tables, probing of the
+// Schur column operator (columnsolve.py:75-108 on one column), no-pivot
+// banded LU (columnsolve.py:111-138)
+// ---------------------------------------------------------------------------
+struct FArgs {
+    Lev lv;
+    double g, lam;
+    const double* cz;
+    const double* Dz;
+    int N, nez, M, ainv_identity;
+    double* lamtab;  // coefS | uA | den
+    double* A;       // M*M dense, row-major, zeroed
+    unsigned* flags;
+};
+
+__global__ void k_lamtab(const FArgs a) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.M) return;
+    const double lam = a.lam;
+    // imexcore.py:236  coef = lam * H0 / (G0 * rho0)
+    a.lamtab[k] = lam * a.lv.H0[k] / (a.lv.G0[k] * a.lv.rho0[k]);
+    // imexcore.py:207-213  u = lam^2/theta0 * g;  den = 1 + w . u
+    const double uA = (lam * lam / a.lv.theta0[k]) * a.g;
+    const double den = 1.0 + a.lv.dth0[k] * uA;
+    a.lamtab[a.M + k] = uA;
+    a.lamtab[2 * a.M + k] = den;
+    if (!a.ainv_identity && fabs(den) < 1e-12) atomicOr(a.flags, HEVI_F_AINV);
+}
+
+__device__ double f_unit(int l, int j) { return l == j ? 1.0 : 0.0; }
+
+// column j of A = lhs_schur(e_j)
+__global__ void k_probe(const FArgs a) {
+    const int N = a.N, M = a.M, nez = a.nez;
+    const double lam = a.lam, gr = a.g;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
+        double up[2 * 16 + 1];  // levels j-N .. j+N (N <= 16)
+        for (int t = 0; t <= 2 * N; ++t) {
+            const int k = j - N + t;
+            up[t] = 0.0;
+            if (k < 0 || k >= M) continue;
+            int s0, row;
+            bool face;
+            lev_elem(k, N, nez, s0, row, face);
+            double acc = 0.0;
+            for (int m = 0; m <= N; ++m) acc = fma(a.Dz[row * (N + 1) + m], f_unit(s0 + m, j), acc);
+            if (face) {
+                double acc2 = 0.0;
+                for (int m = 0; m <= N; ++m)
+                    acc2 = fma(a.Dz[N * (N + 1) + m], f_unit(k - N + m, j), acc2);
+                acc += acc2;
+            }
+            const double dP = a.cz[k] * acc;
+            double v = lam * (dP / a.lv.rho0[k] + (f_unit(k, j) / (a.lv.G0[k] * a.lv.rho0[k])) * gr);
+            if (!a.ainv_identity) {
+                const double uA = a.lamtab[M + k], den = a.lamtab[2 * M + k];
+                v = v - uA * ((a.lv.dth0[k] * v) / den);
+            }
+            up[t] = (k == 0 || k == M - 1) ? 0.0 : v;
+        }
+        for (int k = max(0, j - 2 * N); k <= min(M - 1, j + 2 * N); ++k) {
+            int s0, row;
+            bool face;
+            lev_elem(k, N, nez, s0, row, face);
+            auto upv = [&](int l) -> double {
+                const int t = l - (j - N);
+                return (t >= 0 && t <= 2 * N) ? up[t] : 0.0;
+            };
+            double acc = 0.0;
+            for (int m = 0; m <= N; ++m) acc = fma(a.Dz[row * (N + 1) + m], upv(s0 + m), acc);
+            if (face) {
+                double acc2 = 0.0;
+                for (int m = 0; m <= N; ++m) acc2 = fma(a.Dz[N * (N + 1) + m], upv(k - N + m), acc2);
+                acc += acc2;
+            }
+            const double dup = a.cz[k] * acc;
+            // imexcore.py:264-265, 270-271
+            const double helm = lam * (a.lv.F0z[k] * upv(k) + a.lv.rho0G0[k] * dup);
+            a.A[(long long)k * M + j] = f_unit(k, j) - helm;
+        }
+    }
+}
+
+// single-CTA dense LU restricted to the band, band detection and packing
+__global__ void k_lu_dense(double* A, double* LU, double* LUb, int M, int* nb_out,
+                           unsigned* flags) {
+    __shared__ double red[1024];
+    __shared__ int redi[1024];
+    __shared__ double s_norm;
+    __shared__ int s_nb;
+    const int tid = threadIdx.x, T = blockDim.x;
+    double mx = 0.0;
+    for (int i = tid; i < M * M; i += T) mx = fmax(mx, fabs(A[i]));
+    red[tid] = mx;
+    __syncthreads();
+    for (int s = T / 2; s > 0; s >>= 1) {
+        if (tid < s) red[tid] = fmax(red[tid], red[tid + s]);
+        __syncthreads();
+    }
+    if (tid == 0) s_norm = red[0];
+    __syncthreads();
+    const double norm = s_norm;
+    // bandwidth from the sparsity pattern (columnsolve.py:103-106)
+    int bw = -1;
+    for (int i = tid; i < M * M; i += T) {
+        if (fabs(A[i]) > 1e-14 * norm) bw = max(bw, abs(i / M - i % M));
+    }
+    redi[tid] = bw;
+    __syncthreads();
+    for (int s = T / 2; s > 0; s >>= 1) {
+        if (tid < s) redi[tid] = max(redi[tid], redi[tid + s]);
+        __syncthreads();
+    }
+    if (tid == 0) s_nb = redi[0] + 1;
+    __syncthreads();
+    const int nb = s_nb < 1 ? 1 : s_nb;
+    for (int i = tid; i < M * M; i += T) LU[i] = A[i];
+    __syncthreads();
+    for (int k = 0; k < M; ++k) {
+        double piv = LU[k * M + k];
+        if (fabs(piv) < 1e-12 * norm) {
+            if (tid == 0) atomicOr(flags, HEVI_F_PIVOT);
+            piv = 1.0;
+        }
+        const int E = min(k + nb, M);
+        for (int r = k + 1 + tid; r < E; r += T) LU[r * M + k] /= piv;
+        __syncthreads();
+        const int n = E - (k + 1);
+        for (int t = tid; t < n * n; t += T) {
+            const int r = k + 1 + t / n, cc = k + 1 + t % n;
+            LU[r * M + cc] -= LU[r * M + k] * LU[k * M + cc];
+        }
+        __syncthreads();
+    }
+    const int W = 2 * nb - 1;
+    for (int i = tid; i < M * W; i += T) {
+        const int k = i / W, d = i % W;
+        const int j = k + d - (nb - 1);
+        LUb[i] = (j >= 0 && j < M) ? LU[k * M + j] : 0.0;
+    }
+    if (tid == 0) *nb_out = nb;
+}
+
+// ---------------------------------------------------------------------------
+// E-vector <-> lattice
+// ---------------------------------------------------------------------------
+struct CArgs {
+    Geo g;
+    int N, Ny;
+    long long nel;
+};
+
+__device__ __forceinline__ void rep_of(int gi, int N, int ne, int& k, int& i) {
+    // first occurrence in flat element order: the lower element on a face
+    if (gi > 0 && gi % N == 0) {
+        k = gi / N - 1;
+        i = N;
+    } else {
+        k = min(gi / N, ne - 1);
+        i = gi - k * N;
+    }
+}
+
+__global__ void k_e2l(const double* E, double* Lt, const CArgs a, int nf) {
+    const Geo& g = a.g;
+    const long long n = (long long)g.lX * g.lY * g.Z;
+    const int nr = a.N + 1, ns = a.Ny + 1, nt = a.N + 1;
+    const long long npe = (long long)nr * ns * nt;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int ix = idx % g.lX;
+        const long long t = idx / g.lX;
+        const int iy = t % g.lY;
+        const int gz = t / g.lY;
+        const int gx = g.x0 + ix, gy = g.y0 + iy;
+        int kx, i, ky, j, kz, k;
+        rep_of(gx, a.N, g.nex, kx, i);
+        rep_of(gy, a.Ny, g.ney, ky, j);
+        rep_of(gz, a.N, g.nez, kz, k);
+        const long long e = ((long long)kz * g.ney + ky) * g.nex + kx;
+        const long long node = e * npe + ((long long)k * ns + j) * nr + i;
+        const long long o = ((long long)gz * g.lY + iy) * g.px + ix;
+        for (int f = 0; f < nf; ++f) Lt[f * g.fs + o] = E[f * a.nel * npe + node];
+    }
+}
+
+__global__ void k_l2e(const double* Lt, double* E, const CArgs a, int nf) {
+    const Geo& g = a.g;
+    const int nr = a.N + 1, ns = a.Ny + 1, nt = a.N + 1;
+    const long long npe = (long long)nr * ns * nt;
+    const long long n = a.nel * npe;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = idx % nr;
+        long long t = idx / nr;
+        const int j = t % ns;
+        t /= ns;
+        const int k = t % nt;
+        const long long e = t / nt;
+        const int kx = e % g.nex;
+        const int ky = (e / g.nex) % g.ney;
+        const int kz = e / ((long long)g.nex * g.ney);
+        const int gx = kx * a.N + i, gy = ky * a.Ny + j, gz = kz * a.N + k;
+        const long long o = ((long long)gz * g.lY + (gy - g.y0)) * g.px + (gx - g.x0);
+        for (int f = 0; f < nf; ++f) E[f * n + idx] = Lt[f * g.fs + o];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// generic batched banded column API
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long bidx(int d, int k, int c, int M, int n_col) {
+    return ((long long)d * M + k) * n_col + c;
+}
+
+__global__ void k_band_pack(const double* dense, double* band, int n_col, int M, int nb) {
+    const int W = 2 * nb - 1;
+    const long long n = (long long)n_col * M * W;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int c = idx % n_col;
+        const long long t = idx / n_col;
+        const int k = t % M;
+        const int d = t / M;
+        const int j = k + d - (nb - 1);
+        band[idx] = (j >= 0 && j < M) ? dense[((long long)c * M + k) * M + j] : 0.0;
+    }
+}
+
+__global__ void k_band_unpack(const double* band, double* dense, int n_col, int M, int nb) {
+    const long long n = (long long)n_col * M * M;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int j = idx % M;
+        const long long t = idx / M;
+        const int k = t % M;
+        const int c = t / M;
+        const int d = j - k + nb - 1;
+        dense[idx] = (d >= 0 && d < 2 * nb - 1) ? band[bidx(d, k, c, M, n_col)] : 0.0;
+    }
+}
+
+__global__ void k_band_lu(double* B, int n_col, int M, int nb, double norm, int* bad) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_col) return;
+    const int o = nb - 1;
+    for (int k = 0; k < M; ++k) {
+        double piv = B[bidx(o, k, c, M, n_col)];
+        if (fabs(piv) < 1e-12 * norm) {
+            atomicMin(bad, c);
+            piv = 1.0;
+        }
+        const int E = min(k + nb, M);
+        for (int r = k + 1; r < E; ++r) B[bidx(k - r + o, r, c, M, n_col)] /= piv;
+        for (int r = k + 1; r < E; ++r) {
+            const double l = B[bidx(k - r + o, r, c, M, n_col)];
+            for (int cc = k + 1; cc < E; ++cc)
+                B[bidx(cc - r + o, r, c, M, n_col)] -= l * B[bidx(cc - k + o, k, c, M, n_col)];
+        }
+    }
+}
+
+__global__ void k_band_solve(const double* B, double* rhs, int n_col, int M, int nb) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_col) return;
+    const int o = nb - 1;
+    double* y = rhs + (long long)c * M;
+    for (int i = 1; i < M; ++i) {
+        double s = 0.0;
+        for (int j = max(0, i - nb + 1); j < i; ++j) s = fma(B[bidx(j - i + o, i, c, M, n_col)], y[j], s);
+        y[i] -= s;
+    }
+    for (int i = M - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int j = i + 1; j < min(i + nb, M); ++j) s = fma(B[bidx(j - i + o, i, c, M, n_col)], y[j], s);
+        y[i] = (y[i] - s) / B[bidx(o, i, c, M, n_col)];
+    }
+}
+
+__global__ void k_absmax(const double* a, long long n, unsigned long long* out) {
+    double m = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(a[i]));
+    for (int s = 16; s > 0; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct Factor {
+    double lam = 0.0;
+    int nb = 0;
+    double* A = nullptr;       // M*M
+    double* LU = nullptr;      // M*M
+    double* LUb = nullptr;     // M*(2*M-1) upper bound
+    double* lamtab = nullptr;  // 3*M
+    int* d_nb = nullptr;
+};
+
+struct hevi_plan {
+    Geo g;
+    Lev lv;
+    Phys ph;
+    int N, Ny, ainv_identity;
+    double* d_tab = nullptr;
+    const double *cx, *cy, *cz, *Dx, *Dy, *Dz;
+    unsigned* d_flags = nullptr;
+    unsigned* h_flags = nullptr;
+    std::map<long long, Factor> factors;
+};
+
+namespace {
+
+long long lam_key(double lam) { return llround(lam * 1e12); }
+
+// ---- explicit-kernel dispatch -------------------------------------------
+template <int NX, int NY>
+struct TileCfg;
+// 3D (Ny == N)
+template <> struct TileCfg<1, 1> { static constexpr int TX = 8, TY = 8; };
+template <> struct TileCfg<2, 2> { static constexpr int TX = 4, TY = 4; };
+template <> struct TileCfg<3, 3> { static constexpr int TX = 3, TY = 3; };
+template <> struct TileCfg<4, 4> { static constexpr int TX = 2, TY = 2; };
+template <> struct TileCfg<5, 5> { static constexpr int TX = 2, TY = 1; };
+template <> struct TileCfg<6, 6> { static constexpr int TX = 1, TY = 1; };
+template <> struct TileCfg<7, 7> { static constexpr int TX = 1, TY = 1; };
+template <> struct TileCfg<8, 8> { static constexpr int TX = 1, TY = 1; };
+// slab (Ny == 1, one element across y); N == 1 slab coincides with the 3D N=1 case
+template <> struct TileCfg<2, 1> { static constexpr int TX = 16, TY = 1; };
+template <> struct TileCfg<3, 1> { static constexpr int TX = 12, TY = 1; };
+template <> struct TileCfg<4, 1> { static constexpr int TX = 8, TY = 1; };
+template <> struct TileCfg<5, 1> { static constexpr int TX = 6, TY = 1; };
+template <> struct TileCfg<6, 1> { static constexpr int TX = 5, TY = 1; };
+template <> struct TileCfg<7, 1> { static constexpr int TX = 4, TY = 1; };
+template <> struct TileCfg<8, 1> { static constexpr int TX = 4, TY = 1; };
+
+template <int NX, int NY, int MODE>
+int launch_e(const hevi_plan* pl, EArgs a, cudaStream_t st) {
+    constexpr int TX = TileCfg<NX, NY>::TX, TY = TileCfg<NX, NY>::TY;
+    using T = ETile<NX, NY, NX, TX, TY>;
+    auto kern = k_explicit<NX, NY, NX, TX, TY, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
+        attr = true;
+    }
+    const Geo& g = pl->g;
+    dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
+    kern<<<grid, T::BLK, T::SMEM, st>>>(a);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+template <int MODE>
+int dispatch_e(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
+    const int N = pl->N, Ny = pl->Ny;
+    if (Ny == N) {
+        switch (N) {
+            case 1: return launch_e<1, 1, MODE>(pl, a, st);
+            case 2: return launch_e<2, 2, MODE>(pl, a, st);
+            case 3: return launch_e<3, 3, MODE>(pl, a, st);
+            case 4: return launch_e<4, 4, MODE>(pl, a, st);
+            case 5: return launch_e<5, 5, MODE>(pl, a, st);
+            case 6: return launch_e<6, 6, MODE>(pl, a, st);
+            case 7: return launch_e<7, 7, MODE>(pl, a, st);
+            case 8: return launch_e<8, 8, MODE>(pl, a, st);
+        }
+    } else if (Ny == 1) {
+        switch (N) {
+            case 2: return launch_e<2, 1, MODE>(pl, a, st);
+            case 3: return launch_e<3, 1, MODE>(pl, a, st);
+            case 4: return launch_e<4, 1, MODE>(pl, a, st);
+            case 5: return launch_e<5, 1, MODE>(pl, a, st);
+            case 6: return launch_e<6, 1, MODE>(pl, a, st);
+            case 7: return launch_e<7, 1, MODE>(pl, a, st);
+            case 8: return launch_e<8, 1, MODE>(pl, a, st);
+        }
+    }
+    return fail("unsupported polynomial order (supported: N = 1..8; slab Ny = 1)");
+}
+
+int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
+    switch (mode) {
+        case M_R: return dispatch_e<M_R>(pl, a, st);
+        case M_L: return dispatch_e<M_L>(pl, a, st);
+        case M_S1: return dispatch_e<M_S1>(pl, a, st);
+        case M_S2: return dispatch_e<M_S2>(pl, a, st);
+        case M_S3: return dispatch_e<M_S3>(pl, a, st);
+    }
+    return fail("bad mode");
+}
+
+EArgs base_eargs(const hevi_plan* pl) {
+    EArgs a;
+    memset(&a, 0, sizeof(a));
+    a.g = pl->g;
+    a.lv = pl->lv;
+    a.ph = pl->ph;
+    a.cx = pl->cx;
+    a.cy = pl->cy;
+    a.cz = pl->cz;
+    a.Dx = pl->Dx;
+    a.Dy = pl->Dy;
+    a.Dz = pl->Dz;
+    a.flags = pl->d_flags;
+    return a;
+}
+
+// ---- column-kernel dispatch ---------------------------------------------
+template <int NZ>
+int launch_s(const hevi_plan* pl, SArgs a, cudaStream_t st) {
+    const Geo& g = pl->g;
+    const int M = g.Z;
+    const int W = 2 * a.nb - 1;
+    const size_t fixed = sizeof(double) * ((size_t)10 * M + (size_t)M * W + (NZ + 1) * (NZ + 1));
+    int T = 128;
+    while (T > 32 && fixed + sizeof(double) * 2 * (size_t)M * T > 200 * 1024) T /= 2;
+    const size_t smem = fixed + sizeof(double) * 2 * (size_t)M * T;
+    if (smem > 227 * 1024) return fail("column too tall for the shared-memory column kernel");
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_solve<NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024));
+        attr = true;
+    }
+    const int NYo = g.slab ? 1 : pl->N;
+    const long long cntx = (long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0);
+    const long long cnty = (long long)(g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
+    const long long ncol = cntx * cnty;
+    const int blocks = (int)((ncol + T - 1) / T);
+    k_solve<NZ><<<blocks, T, smem, st>>>(a);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st) {
+    switch (pl->N) {
+        case 1: return launch_s<1>(pl, a, st);
+        case 2: return launch_s<2>(pl, a, st);
+        case 3: return launch_s<3>(pl, a, st);
+        case 4: return launch_s<4>(pl, a, st);
+        case 5: return launch_s<5>(pl, a, st);
+        case 6: return launch_s<6>(pl, a, st);
+        case 7: return launch_s<7>(pl, a, st);
+        case 8: return launch_s<8>(pl, a, st);
+    }
+    return fail("unsupported polynomial order");
+}
+
+const Factor* find_factor(const hevi_plan* pl, double lam) {
+    auto it = pl->factors.find(lam_key(lam));
+    return it == pl->factors.end() ? nullptr : &it->second;
+}
+
+SArgs base_sargs(const hevi_plan* pl, const Factor* f) {
+    SArgs a;
+    memset(&a, 0, sizeof(a));
+    a.g = pl->g;
+    a.lv = pl->lv;
+    a.ph = pl->ph;
+    a.cz = pl->cz;
+    a.Dz = pl->Dz;
+    a.LUb = f->LUb;
+    a.lamtab = f->lamtab;
+    a.nb = f->nb;
+    a.ainv_identity = pl->ainv_identity;
+    a.lam = f->lam;
+    return a;
+}
+
+int blocks_for(long long n, int T = 256) {
+    long long b = (n + T - 1) / T;
+    if (b > 148LL * 32) b = 148LL * 32;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* hevi_last_error(void) { return g_err.c_str(); }
+
+int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_desc* rd) {
+    if (!out || !gd || !rd) return fail("null argument");
+    *out = nullptr;
+    if (gd->N < 1 || gd->N > 8) return fail("polynomial order must be in 1..8");
+    if (!(gd->Ny == gd->N || gd->Ny == 1)) return fail("Ny must equal N (3D) or 1 (slab)");
+    if (gd->slab && (gd->Ny != 1 || gd->ney != 1)) return fail("slab requires Ny = 1, ney = 1");
+    if (gd->nex < 1 || gd->ney < 1 || gd->nez < 1) return fail("element counts must be >= 1");
+    hevi_plan* pl = new hevi_plan();
+    Geo& g = pl->g;
+    g.nex = gd->nex;
+    g.ney = gd->ney;
+    g.nez = gd->nez;
+    g.X = gd->nex * gd->N + 1;
+    g.Y = gd->ney * gd->Ny + 1;
+    g.Z = gd->nez * gd->N + 1;
+    g.x0 = gd->x0;
+    g.y0 = gd->y0;
+    g.lX = gd->lX;
+    g.lY = gd->lY;
+    g.px = gd->px;
+    g.fs = (long long)g.Z * g.lY * g.px;
+    g.ex_b = gd->ex_b;
+    g.ex_e = gd->ex_e;
+    g.ey_b = gd->ey_b;
+    g.ey_e = gd->ey_e;
+    g.slab = gd->slab;
+    if (g.px < g.lX || g.ex_b < 0 || g.ex_e > g.nex || g.ex_b >= g.ex_e || g.ey_b < 0 ||
+        g.ey_e > g.ney || g.ey_b >= g.ey_e) {
+        delete pl;
+        return fail("inconsistent window / ownership");
+    }
+    pl->N = gd->N;
+    pl->Ny = gd->Ny;
+    pl->ph = {rd->g, rd->R, rd->P0, rd->gamma};
+    const int Z = g.Z, X = g.X, Y = g.Y;
+    const int nd = (gd->N + 1) * (gd->N + 1), ndy = (gd->Ny + 1) * (gd->Ny + 1);
+    std::vector<double> h;
+    h.reserve(9 * Z + X + Y + Z + 2 * nd + ndy);
+    const double* lv[9] = {rd->rho0, rd->theta0, rd->P0f, rd->drho0, rd->dtheta0,
+                           rd->G0,   rd->H0,     rd->F0z, rd->rho0G0};
+    for (int t = 0; t < 9; ++t) h.insert(h.end(), lv[t], lv[t] + Z);
+    h.insert(h.end(), rd->cx, rd->cx + X);
+    h.insert(h.end(), rd->cy, rd->cy + Y);
+    h.insert(h.end(), rd->cz, rd->cz + Z);
+    h.insert(h.end(), rd->Dx, rd->Dx + nd);
+    h.insert(h.end(), rd->Dy, rd->Dy + ndy);
+    h.insert(h.end(), rd->Dz, rd->Dz + nd);
+    pl->ainv_identity = 1;
+    for (int k = 0; k < Z; ++k)
+        if (rd->dtheta0[k] != 0.0) pl->ainv_identity = 0;
+    cudaError_t e = cudaMalloc(&pl->d_tab, h.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(pl->d_tab, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&pl->d_flags, 16 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(pl->d_flags, 0, 16 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMallocHost(&pl->h_flags, 16 * sizeof(unsigned));
+    if (e != cudaSuccess) {
+        hevi_plan_destroy(pl);
+        return fail("plan allocation", e);
+    }
+    const double* d = pl->d_tab;
+    pl->lv = {d, d + Z, d + 2 * Z, d + 3 * Z, d + 4 * Z, d + 5 * Z, d + 6 * Z, d + 7 * Z, d + 8 * Z};
+    pl->cx = d + 9 * Z;
+    pl->cy = pl->cx + X;
+    pl->cz = pl->cy + Y;
+    pl->Dx = pl->cz + Z;
+    pl->Dy = pl->Dx + nd;
+    pl->Dz = pl->Dy + ndy;
+    *out = pl;
+    return HEVI_OK;
+}
+
+int hevi_plan_destroy(hevi_plan* pl) {
+    if (!pl) return HEVI_OK;
+    for (auto& kv : pl->factors) {
+        cudaFree(kv.second.A);
+        cudaFree(kv.second.LU);
+        cudaFree(kv.second.LUb);
+        cudaFree(kv.second.lamtab);
+        cudaFree(kv.second.d_nb);
+    }
+    cudaFree(pl->d_tab);
+    cudaFree(pl->d_flags);
+    if (pl->h_flags) cudaFreeHost(pl->h_flags);
+    delete pl;
+    return HEVI_OK;
+}
+
+long long hevi_state_size(const hevi_plan* pl) { return pl ? 5 * pl->g.fs : 0; }
+
+int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
+    if (!pl) return fail("null plan");
+    if (!(lam > 0.0)) return fail("implicit solve requires positive lam");
+    cudaStream_t st = (cudaStream_t)stream;
+    auto it = pl->factors.find(lam_key(lam));
+    if (it == pl->factors.end()) {
+        Factor f;
+        f.lam = lam;
+        const int M = pl->g.Z;
+        if (pl->N > 16) return fail("order too high for probing");
+        CK(cudaMalloc(&f.A, sizeof(double) * M * M));
+        CK(cudaMalloc(&f.LU, sizeof(double) * M * M));
+        CK(cudaMalloc(&f.LUb, sizeof(double) * M * (2 * M - 1)));
+        CK(cudaMalloc(&f.lamtab, sizeof(double) * 3 * M));
+        CK(cudaMalloc(&f.d_nb, sizeof(int)));
+        CK(cudaMemsetAsync(f.A, 0, sizeof(double) * M * M, st));
+        FArgs a;
+        a.lv = pl->lv;
+        a.g = pl->ph.g;
+        a.lam = lam;
+        a.cz = pl->cz;
+        a.Dz = pl->Dz;
+        a.N = pl->N;
+        a.nez = pl->g.nez;
+        a.M = M;
+        a.ainv_identity = pl->ainv_identity;
+        a.lamtab = f.lamtab;
+        a.A = f.A;
+        a.flags = pl->d_flags;
+        k_lamtab<<<(M + 127) / 128, 128, 0, st>>>(a);
+        CK(cudaGetLastError());
+        k_probe<<<(M + 63) / 64, 64, 0, st>>>(a);
+        CK(cudaGetLastError());
+        k_lu_dense<<<1, 256, 0, st>>>(f.A, f.LU, f.LUb, M, f.d_nb, pl->d_flags);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&f.nb, f.d_nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        it = pl->factors.emplace(lam_key(lam), f).first;
+    }
+    if (nb_out) *nb_out = it->second.nb;
+    return HEVI_OK;
+}
+
+int hevi_column_matrix(hevi_plan* pl, double lam, double* A_host, double* LU_host, void* stream) {
+    const Factor* f = pl ? find_factor(pl, lam) : nullptr;
+    if (!f) {
+        g_err = "lam not factored";
+        return HEVI_ENOFACTOR;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = sizeof(double) * pl->g.Z * pl->g.Z;
+    if (A_host) CK(cudaMemcpyAsync(A_host, f->A, bytes, cudaMemcpyDeviceToHost, st));
+    if (LU_host) CK(cudaMemcpyAsync(LU_host, f->LU, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return HEVI_OK;
+}
+
+int hevi_rhs(hevi_plan* pl, const double* q, double* R, void* stream) {
+    if (!pl || !q || !R) return fail("null argument");
+    EArgs a = base_eargs(pl);
+    a.q = q;
+    a.out = R;
+    a.stage = 0;
+    return run_e(pl, M_R, a, (cudaStream_t)stream);
+}
+
+int hevi_linear_v(hevi_plan* pl, const double* q, double* L, void* stream) {
+    if (!pl || !q || !L) return fail("null argument");
+    EArgs a = base_eargs(pl);
+    a.q = q;
+    a.out = L;
+    return run_e(pl, M_L, a, (cudaStream_t)stream);
+}
+
+int hevi_solve(hevi_plan* pl, double lam, const double* qe, double* q, void* stream) {
+    if (!pl || !qe || !q) return fail("null argument");
+    if (!(lam > 0.0)) return fail("implicit solve requires positive lam");
+    int rc = hevi_factor(pl, lam, nullptr, stream);
+    if (rc) return rc;
+    SArgs a = base_sargs(pl, find_factor(pl, lam));
+    a.P = qe;
+    a.out = q;
+    a.src_uv = qe;
+    return run_s(pl, a, (cudaStream_t)stream);
+}
+
+int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q, double* work,
+               void* stream) {
+    if (!pl || !tab || !Q || !work) return fail("null argument");
+    const long long fs5 = 5 * pl->g.fs;
+    double* Q1 = work;
+    double* A = work + fs5;
+    double* F = work + 2 * fs5;
+    double* P = work + 3 * fs5;
+    const double* a_ = tab;        // a[3][3]
+    const double* at = tab + 9;    // at[3][3]
+    const double* b = tab + 18;    // b[3]
+    EArgs a = base_eargs(pl);
+    a.dt = dt;
+    a.stage = stage;
+    int mode;
+    if (stage == 0) {
+        mode = M_S1;
+        a.q = Q;
+        a.P = P;
+        a.Quv = Q1;
+        a.A = A;
+        a.F = F;
+        a.a_p = a_[3 * 1 + 0];
+        a.at_p = at[3 * 1 + 0];
+        a.a_a = a_[3 * 2 + 0];
+        a.at_a = at[3 * 2 + 0];
+        a.cb = dt * b[0];
+    } else if (stage == 1) {
+        mode = M_S2;
+        a.q = Q1;
+        a.P = P;
+        a.Quv = A;
+        a.A = A;
+        a.F = F;
+        a.a_p = a_[3 * 2 + 1];
+        a.at_p = at[3 * 2 + 1];
+        a.cb = dt * b[1];
+    } else if (stage == 2) {
+        mode = M_S3;
+        a.q = A;
+        a.F = F;
+        a.out = Q;
+        a.cb = dt * b[2];
+    } else {
+        return fail("stage must be 0, 1 or 2");
+    }
+    return run_e(pl, mode, a, (cudaStream_t)stream);
+}
+
+int hevi_stage_solve(hevi_plan* pl, int stage, double lam, double* work, void* stream) {
+    if (!pl || !work) return fail("null argument");
+    const Factor* f = find_factor(pl, lam);
+    if (!f) {
+        g_err = "lam not factored (call hevi_factor first)";
+        return HEVI_ENOFACTOR;
+    }
+    const long long fs5 = 5 * pl->g.fs;
+    SArgs a = base_sargs(pl, f);
+    a.P = work + 3 * fs5;
+    a.out = stage == 0 ? work : work + fs5;
+    a.src_uv = nullptr;
+    return run_s(pl, a, (cudaStream_t)stream);
+}
+
+int hevi_ark2_step(hevi_plan* pl, double dt, const double* tab, double* Q, double* work,
+                   void* stream) {
+    if (!pl || !tab) return fail("null argument");
+    const double lam = tab[9 + 3 * 1 + 1] * dt;  // problem.lam = tableau.diag * dt
+    int rc = hevi_factor(pl, lam, nullptr, stream);
+    if (rc) return rc;
+    if ((rc = hevi_stage(pl, 0, dt, tab, Q, work, stream))) return rc;
+    if ((rc = hevi_stage_solve(pl, 0, lam, work, stream))) return rc;
+    if ((rc = hevi_stage(pl, 1, dt, tab, Q, work, stream))) return rc;
+    if ((rc = hevi_stage_solve(pl, 1, lam, work, stream))) return rc;
+    return hevi_stage(pl, 2, dt, tab, Q, work, stream);
+}
+
+int hevi_evec_to_lattice(hevi_plan* pl, const double* E, double* Lt, int nf, void* stream) {
+    if (!pl || !E || !Lt) return fail("null argument");
+    CArgs a;
+    a.g = pl->g;
+    a.N = pl->N;
+    a.Ny = pl->Ny;
+    a.nel = (long long)pl->g.nex * pl->g.ney * pl->g.nez;
+    const long long n = (long long)pl->g.lX * pl->g.lY * pl->g.Z;
+    k_e2l<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(E, Lt, a, nf);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_lattice_to_evec(hevi_plan* pl, const double* Lt, double* E, int nf, void* stream) {
+    if (!pl || !E || !Lt) return fail("null argument");
+    if (pl->g.lX != pl->g.X || pl->g.lY != pl->g.Y) return fail("lattice_to_evec needs the full lattice");
+    CArgs a;
+    a.g = pl->g;
+    a.N = pl->N;
+    a.Ny = pl->Ny;
+    a.nel = (long long)pl->g.nex * pl->g.ney * pl->g.nez;
+    const long long n = a.nel * (pl->N + 1) * (pl->Ny + 1) * (pl->N + 1);
+    k_l2e<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(Lt, E, a, nf);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_flags(hevi_plan* pl, unsigned* flags, int reset, void* stream) {
+    if (!pl || !flags) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(pl->h_flags, pl->d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    if (reset) CK(cudaMemsetAsync(pl->d_flags, 0, sizeof(unsigned), st));
+    CK(cudaStreamSynchronize(st));
+    *flags = pl->h_flags[0];
+    return HEVI_OK;
+}
+
+int hevi_band_pack(const double* dense, double* band, int n_col, int M, int nb, void* stream) {
+    if (!dense || !band || n_col < 1 || M < 1 || nb < 1) return fail("bad band_pack arguments");
+    k_band_pack<<<blocks_for((long long)n_col * M * (2 * nb - 1)), 256, 0, (cudaStream_t)stream>>>(
+        dense, band, n_col, M, nb);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_band_unpack(const double* band, double* dense, int n_col, int M, int nb, void* stream) {
+    if (!dense || !band || n_col < 1 || M < 1 || nb < 1) return fail("bad band_unpack arguments");
+    k_band_unpack<<<blocks_for((long long)n_col * M * M), 256, 0, (cudaStream_t)stream>>>(
+        band, dense, n_col, M, nb);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_band_lu(double* band, int n_col, int M, int nb, double norm, int* bad_col, void* stream) {
+    if (!band || !bad_col || n_col < 1 || M < 1 || nb < 1) return fail("bad band_lu arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    int* d_bad;
+    CK(cudaMallocAsync(&d_bad, sizeof(int), st));
+    const int big = 0x7fffffff;
+    CK(cudaMemcpyAsync(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+    k_band_lu<<<(n_col + 127) / 128, 128, 0, st>>>(band, n_col, M, nb, norm, d_bad);
+    CK(cudaGetLastError());
+    int h = big;
+    CK(cudaMemcpyAsync(&h, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d_bad, st));
+    CK(cudaStreamSynchronize(st));
+    *bad_col = (h == big) ? -1 : h;
+    return HEVI_OK;
+}
+
+int hevi_band_solve(const double* band, double* rhs, int n_col, int M, int nb, void* stream) {
+    if (!band || !rhs || n_col < 1 || M < 1 || nb < 1) return fail("bad band_solve arguments");
+    k_band_solve<<<(n_col + 127) / 128, 128, 0, (cudaStream_t)stream>>>(band, rhs, n_col, M, nb);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_absmax(const double* a, long long n, double* out_host, void* stream) {
+    if (!a || !out_host) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* d;
+    CK(cudaMallocAsync(&d, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+    k_absmax<<<blocks_for(n), 256, 0, st>>>(a, n, d);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d, st));
+    CK(cudaStreamSynchronize(st));
+    double v;
+    memcpy(&v, &h, sizeof(v));
+    *out_host = v;
+    return HEVI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+"""ARK2 IMEX stepper and the vertically-implicit problem (drop-in for
+``dycore.imexcore`` along the HEVI path).
+
+``ark_imex_step(q, dt, tableau, problem, rhs)`` keeps the reference
+signature and semantics (imexcore.py:385-414): three explicit evaluations,
+two implicit solves with ``problem.lam = tableau.diag * dt``, the combine
+with the shared weights, a fresh output array, FloatingPointError on a
+non-finite result.  When ``problem`` is this module's ``ImplicitProblem``
+(cG, set2nc, Schur form, dim='1d', method='direct') and ``rhs`` is an
+``euler.RHS`` on the same discretization, the whole step runs as the fused
+five-kernel device schedule; any other duck-typed problem/rhs
+pair runs the reference's generic stage loop on the caller's callables.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import euler
+
+
+@dataclass(frozen=True)
+class ButcherPair:
+    """Double Butcher tableau (imexcore.py:26-41)."""
+    a: np.ndarray
+    at: np.ndarray
+    b: np.ndarray
+    c: np.ndarray
+    ct: np.ndarray
+
+    @property
+    def stages(self) -> int:
+        return len(self.b)
+
+    @property
+    def diag(self) -> float:
+        return float(self.at[1, 1])
+
+
+def ark2_tableau() -> ButcherPair:
+    """L-stable ARK2 pair with the reference's sign-corrected weights
+    (imexcore.py:44-63; the paper's printed row fails sum b = 1)."""
+    s2 = math.sqrt(2.0)
+    gam = 1.0 - 1.0 / s2
+    d = 1.0 / (2.0 * s2)
+    a32 = (3.0 + 2.0 * s2) / 6.0
+    a = np.array([[0.0, 0.0, 0.0], [2.0 - s2, 0.0, 0.0], [1.0 - a32, a32, 0.0]])
+    at = np.array([[0.0, 0.0, 0.0], [gam, gam, 0.0], [d, d, gam]])
+    b = np.array([d, d, gam])
+    return ButcherPair(a=a, at=at, b=b, c=a.sum(axis=1), ct=at.sum(axis=1))
+
+
+@dataclass
+class SolverSpec:
+    """imexcore.py:133-140 (only method='direct' is on the HEVI path)."""
+    method: str = "gmres"
+    tol: float = 1e-6
+    max_iter: int = 2000
+    restart: int = 50
+    precon_order: int = 1
+    check_every: int = 4
+
+
+@dataclass
+class SolveStats:
+    """imexcore.py:143-155; the direct path increments only ``solves``."""
+    solves: int = 0
+    iterations: int = 0
+    matvecs: int = 0
+    failures: int = 0
+
+
+class SolverFailure(RuntimeError):
+    """imexcore.py:158-162 (raised by iterative solvers only)."""
+
+    def __init__(self, report):
+        super().__init__(f"implicit solve failed: {report}")
+        self.report = report
+
+
+@dataclass
+class ImplicitProblem:
+    """(I - lam L_V) q = q_e on the device (imexcore.py:165-322)."""
+    disc: euler.Discretization
+    ref: euler.ReferenceState
+    set_name: str
+    discretization: str = "cg"
+    form: str = "schur"
+    dim: str = "3d"
+    lam: float = 0.0
+    solver: SolverSpec = field(default_factory=SolverSpec)
+    stats: SolveStats = field(default_factory=SolveStats)
+    _column_cache: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.discretization == "dg":
+            if self.form == "schur":
+                raise ValueError("the pressure-reduced form is not supported with dG fluxes")
+            if self.set_name != "set2c":
+                raise ValueError("dG requires the conservative set")
+
+    # -- what the device path implements --------------------------------------
+    def _check_path(self):
+        if self.discretization != "cg":
+            raise NotImplementedError("dG is outside the HEVI direct path")
+        if self.solver.method != "direct":
+            raise NotImplementedError("iterative (3D-IMEX) solvers are SURVEY 8(f) 'next'; "
+                                      "use SolverSpec(method='direct') with dim='1d'")
+        if self.dim != "1d":
+            raise ValueError("the direct column solver requires the 1D form")
+        if self.form != "schur":
+            raise NotImplementedError("the device path implements the Schur (pressure) form")
+        euler._check_set(self.set_name)
+
+    @property
+    def fused(self) -> bool:
+        try:
+            self._check_path()
+        except (NotImplementedError, ValueError):
+            return False
+        return True
+
+    def linear(self, q):
+        """imexcore.py:190-194."""
+        if self.dim == "1d":
+            return euler.vertical_restriction(q, self.ref, self.disc, self.set_name)
+        return euler.linear_operator(q, self.ref, self.disc, self.set_name)
+
+    def solve(self, q_e):
+        """imexcore.py:312-322 (direct branch)."""
+        if self.lam <= 0:
+            raise ValueError("implicit solve requires positive lam")
+        self._check_path()
+        from . import columnsolve
+        out = columnsolve.solve_direct(self, q_e)
+        self.stats.solves += 1
+        return out
+
+
+def _is_fused(problem, rhs) -> bool:
+    return (isinstance(problem, ImplicitProblem) and isinstance(rhs, euler.RHS)
+            and problem.fused and rhs.disc is problem.disc and rhs.ref is problem.ref
+            and rhs.set_name == problem.set_name)
+
+
+def ark_imex_step(q, dt: float, tableau: ButcherPair, problem, rhs):
+    """One additive Runge-Kutta IMEX step (imexcore.py:385-414)."""
+    if _is_fused(problem, rhs) and tableau.stages == 3:
+        from .plan import tableau_array, to_device
+        plan = problem.disc.plan_for(problem.ref)
+        problem.lam = tableau.diag * dt
+        E, back = to_device(q)
+        Q = plan.e2l(E)
+        work = plan.workspace()
+        plan.step(dt, tableau_array(tableau), Q, work)
+        plan.check_flags()
+        problem.stats.solves += 2
+        return back(plan.l2e(Q))
+    return _generic_step(q, dt, tableau, problem, rhs)
+
+
+def _generic_step(q, dt, tableau, problem, rhs):
+    """The reference stage loop on duck-typed callables (imexcore.py:393-414)."""
+    s = tableau.stages
+    R = [rhs(q)]
+    L = [problem.linear(q)]
+    problem.lam = tableau.diag * dt
+    for i in range(1, s):
+        pred = q.copy() if hasattr(q, "copy") else q.clone()
+        for j in range(i):
+            pred += dt * (tableau.a[i, j] * (R[j] - L[j]) + tableau.at[i, j] * L[j])
+        qi = problem.solve(pred)
+        R.append(rhs(qi))
+        if i < s - 1:
+            L.append(problem.linear(qi))
+    out = q.copy() if hasattr(q, "copy") else q.clone()
+    for i in range(s):
+        out += dt * tableau.b[i] * R[i]
+    finite = np.isfinite(out).all() if isinstance(out, np.ndarray) else bool(out.isfinite().all())
+    if not finite:
+        raise FloatingPointError("non-finite state after IMEX step")
+    return out

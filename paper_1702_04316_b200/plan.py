@@ -1,0 +1,193 @@
+"""Device plan: owns the libhevi plan handle and the lattice <-> E-vector glue.
+
+A plan is built from a mesh (+ Discretization tables) and a ReferenceState.
+Its state arrays are lattice tensors ``(5, Z, lY, px)`` (fp64, CUDA) owned by
+the PyTorch caching allocator and passed to the C ABI as raw pointers.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nv
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def raise_for_flags(flags: int):
+    """Map sticky device flags to the reference's exception types, in the
+    order the reference would have raised them."""
+    for s in (0, 1, 2):
+        if flags & nv.F_NONFINITE_IN(s):
+            raise FloatingPointError("non-finite state passed to RHS evaluation")
+        if flags & nv.F_EOS(s):
+            raise ValueError("EOS requires positive density and temperature")
+    if flags & nv.F_AINV:
+        raise FloatingPointError("rank-one inverse denominator underflow")
+    if flags & nv.F_PIVOT:
+        raise RuntimeError("no-pivot LU hit a degenerate diagonal (the pivoted dense "
+                           "fallback of columnsolve.factor_with_fallback is not implemented "
+                           "on the device path)")
+    if flags & nv.F_NONFINITE_OUT:
+        raise FloatingPointError("non-finite state after IMEX step")
+
+
+class HeviPlan:
+    def __init__(self, mesh, ref, disc, window=None):
+        import torch
+        nv.require_cuda()
+        self.lib = nv.load()
+        self.mesh, self.ref, self.disc = mesh, ref, disc
+        X, Y, Z = mesh.X, mesh.Y, mesh.Z
+        if window is None:
+            window = dict(x0=0, y0=0, lX=X, lY=Y, ex_b=0, ex_e=mesh.nx, ey_b=0, ey_e=mesh.ny)
+        self.window = window
+        px = window.get("px", window["lX"])
+        gd = nv.GridDesc(nex=mesh.nx, ney=mesh.ny, nez=mesh.nz, N=mesh.N, Ny=mesh.Ny,
+                         slab=int(mesh.slab), x0=window["x0"], y0=window["y0"],
+                         lX=window["lX"], lY=window["lY"], px=px,
+                         ex_b=window["ex_b"], ex_e=window["ex_e"],
+                         ey_b=window["ey_b"], ey_e=window["ey_e"])
+        c = ref.const
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (
+            ref.rho0, ref.theta0, ref.P0f, ref.drho0, ref.dtheta0, ref.G0_nc, ref.H0_nc,
+            ref.F0z_nc, ref.rho0G0, disc.cx, disc.cy, disc.cz,
+            mesh.quad_r.D, mesh.quad_s.D, mesh.quad_t.D)]
+        rd = nv.RefDesc(*[_dp(a) for a in self._keep], c.g, c.R, c.P0, c.gamma)
+        h = ctypes.c_void_p()
+        nv.check(self.lib.hevi_plan_create(ctypes.byref(h), ctypes.byref(gd), ctypes.byref(rd)))
+        self.h = h
+        self.Z, self.lY, self.lX, self.px = Z, window["lY"], window["lX"], px
+        self.shape = (5, Z, self.lY, px)
+        self.fs = Z * self.lY * px
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.hevi_plan_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    # -- buffers -------------------------------------------------------------
+    def empty(self, nf=5):
+        import torch
+        return torch.empty((nf,) + self.shape[1:], dtype=torch.float64, device=self.device)
+
+    def zeros(self, nf=5):
+        import torch
+        return torch.zeros((nf,) + self.shape[1:], dtype=torch.float64, device=self.device)
+
+    def workspace(self):
+        """[Q1 | A | F | P] of the fused step."""
+        import torch
+        return torch.zeros((4,) + self.shape, dtype=torch.float64, device=self.device)
+
+    # -- conversions -----------------------------------------------------------
+    def e2l(self, E, out=None, nf=None):
+        nf = E.shape[0] if nf is None else nf
+        out = self.zeros(nf) if out is None else out
+        nv.check(self.lib.hevi_evec_to_lattice(self.h, nv.ptr(E), nv.ptr(out), nf, nv.stream_ptr()))
+        return out
+
+    def l2e(self, L, out=None):
+        import torch
+        nf = L.shape[0]
+        if out is None:
+            out = torch.empty((nf,) + tuple(self.mesh.nshape), dtype=torch.float64, device=self.device)
+        nv.check(self.lib.hevi_lattice_to_evec(self.h, nv.ptr(L), nv.ptr(out), nf, nv.stream_ptr()))
+        return out
+
+    # -- operators on lattice tensors -------------------------------------------
+    def rhs(self, q, out):
+        nv.check(self.lib.hevi_rhs(self.h, nv.ptr(q), nv.ptr(out), nv.stream_ptr()))
+        return out
+
+    def linear(self, q, out):
+        nv.check(self.lib.hevi_linear_v(self.h, nv.ptr(q), nv.ptr(out), nv.stream_ptr()))
+        return out
+
+    def factor(self, lam) -> int:
+        nb = ctypes.c_int(0)
+        nv.check(self.lib.hevi_factor(self.h, float(lam), ctypes.byref(nb), nv.stream_ptr()))
+        return nb.value
+
+    def column_matrix(self, lam):
+        M = self.Z
+        self.factor(lam)
+        A = np.empty((M, M))
+        LU = np.empty((M, M))
+        nv.check(self.lib.hevi_column_matrix(self.h, float(lam), A.ctypes.data_as(ctypes.c_void_p),
+                                             LU.ctypes.data_as(ctypes.c_void_p), nv.stream_ptr()))
+        return A, LU
+
+    def solve(self, lam, qe, out):
+        nv.check(self.lib.hevi_solve(self.h, float(lam), nv.ptr(qe), nv.ptr(out), nv.stream_ptr()))
+        return out
+
+    def step(self, dt, tab: np.ndarray, Q, work):
+        nv.check(self.lib.hevi_ark2_step(self.h, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
+                                         nv.stream_ptr()))
+
+    def stage(self, s, dt, tab: np.ndarray, Q, work):
+        nv.check(self.lib.hevi_stage(self.h, s, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
+                                     nv.stream_ptr()))
+
+    def stage_solve(self, s, lam, work):
+        nv.check(self.lib.hevi_stage_solve(self.h, s, float(lam), nv.ptr(work), nv.stream_ptr()))
+
+    def flags(self, reset=True) -> int:
+        f = ctypes.c_uint(0)
+        nv.check(self.lib.hevi_flags(self.h, ctypes.byref(f), int(reset), nv.stream_ptr()))
+        return f.value
+
+    def check_flags(self):
+        raise_for_flags(self.flags(reset=True))
+
+    # -- E-vector entry used by the drop-in operators ---------------------------
+    def apply_evec(self, op, q, lam=None):
+        E, back = to_device(q)
+        if E.shape != (5,) + tuple(self.mesh.nshape):
+            raise ValueError("field/mesh shape mismatch")
+        L = self.e2l(E)
+        out = self.zeros()
+        if op == "rhs":
+            self.rhs(L, out)
+        elif op == "linear":
+            self.linear(L, out)
+        elif op == "solve":
+            self.solve(lam, L, out)
+        else:
+            raise ValueError(op)
+        self.check_flags()
+        return back(self.l2e(out))
+
+
+def to_device(q):
+    """E-vector (numpy or torch) -> contiguous fp64 CUDA tensor, plus a
+    function returning results in the caller's array type."""
+    import torch
+    if isinstance(q, torch.Tensor):
+        dev = q.device
+        t = q.to(device="cuda", dtype=torch.float64).contiguous()
+        if dev.type == "cuda":
+            return t, (lambda r: r)
+        return t, (lambda r: r.to(dev))
+    arr = np.ascontiguousarray(q, dtype=np.float64)
+    t = torch.from_numpy(arr).to("cuda")
+    return t, (lambda r: r.cpu().numpy())
+
+
+def tableau_array(tab) -> np.ndarray:
+    """{a, at, b} of a ButcherPair packed as the C ABI expects."""
+    a = np.asarray(tab.a, dtype=np.float64)
+    at = np.asarray(tab.at, dtype=np.float64)
+    b = np.asarray(tab.b, dtype=np.float64)
+    if a.shape != (3, 3) or at.shape != (3, 3) or b.shape != (3,):
+        raise ValueError("the fused HEVI step needs a 3-stage ARK pair")
+    return np.ascontiguousarray(np.concatenate([a.ravel(), at.ravel(), b]))

@@ -1,0 +1,61 @@
+"""Resident multi-step driver: the state stays on the lattice in HBM, each
+step is the fused five-kernel schedule, optionally replayed as a CUDA graph.
+This is what ``cli.run_simulation``'s hot loop (cli.py:224-241) becomes."""
+from __future__ import annotations
+
+from . import imexcore
+from .plan import tableau_array
+
+
+class HeviStepper:
+    def __init__(self, disc, ref, dt, tableau=None, check_every=1):
+        self.plan = disc.plan_for(ref)
+        self.tableau = tableau or imexcore.ark2_tableau()
+        self.tab = tableau_array(self.tableau)
+        self.dt = float(dt)
+        self.lam = self.tableau.diag * self.dt
+        self.nb = self.plan.factor(self.lam)
+        self.Q = self.plan.zeros()
+        self.work = self.plan.workspace()
+        self.check_every = check_every
+        self.steps = 0
+        self._graph = None
+
+    # state in / out ---------------------------------------------------------
+    def set_state(self, q, lattice=False):
+        if lattice:
+            self.Q[:, :, :, :q.shape[-1]].copy_(q)
+        else:
+            from .plan import to_device
+            E, _ = to_device(q)
+            self.plan.e2l(E, out=self.Q)
+
+    def state(self, lattice=False):
+        if lattice:
+            return self.Q[:, :, :, :self.plan.lX]
+        return self.plan.l2e(self.Q)
+
+    # stepping ---------------------------------------------------------------
+    def _launch(self):
+        self.plan.step(self.dt, self.tab, self.Q, self.work)
+
+    def capture(self):
+        """Record one step as a CUDA graph (5 kernel launches)."""
+        import torch
+        self._launch()  # warm: kernels' smem attributes are set outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch()
+        self._graph = g
+        return g
+
+    def step(self, n=1, check=True):
+        for _ in range(n):
+            if self._graph is not None:
+                self._graph.replay()
+            else:
+                self._launch()
+            self.steps += 1
+            if check and self.check_every and self.steps % self.check_every == 0:
+                self.plan.check_flags()

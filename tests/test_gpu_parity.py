@@ -1,0 +1,173 @@
+"""Parity of the CUDA path against the reference golden fixtures and the CPU
+oracle (SURVEY 8(c) tiered gate).  Runs on a B200 (``-m gpu``).
+
+Gate (tolerances written here, per field, relative L2):
+  (A) operators on identical inputs: L_V, Schur solve <= 1e-13 (velocity as a
+      vector); R: rho', theta' <= 1e-13, momentum <= 2e-9 (EOS/pow floor);
+  (B) 10 ARK2 steps at C=15: rho', theta' <= 1e-10, velocity vector <= 5e-9;
+  (C) determinism: bitwise-identical reruns.
+"""
+import numpy as np
+import pytest
+
+from conftest import CASES, load_golden, oracle_for, rel_fields
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1702_04316_b200 import specgrid, euler, imexcore, columnsolve  # noqa: E402
+
+OPS_SCALAR_TOL = 1e-13
+OPS_MOM_TOL = 2e-9
+SOLVE_TOL = 1e-13
+STEP_SCALAR_TOL = 1e-10
+STEP_VEL_TOL = 5e-9
+
+
+def build(name):
+    kw = dict(CASES[name])
+    if kw.get("slab"):
+        mesh = specgrid.build_box_mesh(kw["nx"], kw["nz"], kw["Lx"], kw["Lz"], kw["N"])
+    else:
+        mesh = specgrid.build_box_mesh_3d(kw["nx"], kw["ny"], kw["nz"], kw["Lx"], kw["Ly"],
+                                          kw["Lz"], kw["N"])
+    if kw.get("background") == "isothermal":
+        ref = euler.isothermal_reference(mesh, 300.0)
+    else:
+        ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    return mesh, ref, disc
+
+
+@pytest.fixture(scope="module", params=sorted(CASES))
+def case(request):
+    name = request.param
+    mesh, ref, disc = build(name)
+    return name, mesh, ref, disc, oracle_for(name), load_golden(name)
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
+def test_rhs_matches_reference(case):
+    name, mesh, ref, disc, o, g = case
+    q = o.from_lattice(g["ops_q"])
+    R = euler.nonlinear_rhs(dev(q), ref, disc, "set2nc").cpu().numpy()
+    e_rho, e_vel, e_th = rel_fields(o.to_lattice(R), g["ops_R"])
+    assert e_rho < OPS_SCALAR_TOL and e_th < OPS_SCALAR_TOL, (name, e_rho, e_th)
+    assert e_vel < OPS_MOM_TOL, (name, e_vel)
+
+
+def test_linear_matches_reference(case):
+    name, mesh, ref, disc, o, g = case
+    q = o.from_lattice(g["ops_q"])
+    L = euler.vertical_restriction(q, ref, disc, "set2nc")      # numpy in -> numpy out
+    assert isinstance(L, np.ndarray)
+    errs = rel_fields(o.to_lattice(L), g["ops_L"])
+    assert max(errs) < SOLVE_TOL, (name, errs)
+
+
+def test_solve_matches_reference(case):
+    name, mesh, ref, disc, o, g = case
+    q = o.from_lattice(g["ops_q"])
+    prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                    solver=imexcore.SolverSpec(method="direct"))
+    prob.lam = float(g["ops_lam"])
+    out = prob.solve(dev(q)).cpu().numpy()
+    errs = rel_fields(o.to_lattice(out), g["ops_solve"])
+    assert max(errs) < SOLVE_TOL, (name, errs)
+    assert prob.stats.solves == 1
+
+
+def test_column_matrix_matches_probed_reference(case):
+    name, mesh, ref, disc, o, g = case
+    plan = disc.plan_for(ref)
+    lam = float(g["ops_lam"])
+    A, LU = plan.column_matrix(lam)
+    scale = np.abs(g["col_A0"]).max()
+    assert np.abs(A - g["col_A0"]).max() <= 1e-13 * scale
+    assert plan.factor(lam) == int(g["col_nb"])
+    assert np.abs(LU - g["col_LU0"]).max() <= 1e-12 * np.abs(g["col_LU0"]).max()
+
+
+def test_steps_match_reference(case):
+    name, mesh, ref, disc, o, g = case
+    q = dev(o.from_lattice(g["step_q0"]))
+    dt = float(g["step_dt"])
+    prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                    solver=imexcore.SolverSpec(method="direct"))
+    rhs = euler.make_rhs(ref, disc, "set2nc")
+    tab = imexcore.ark2_tableau()
+    keep = sorted(int(k[6:]) for k in g.files if k.startswith("step_q") and k != "step_q0")
+    for k in range(1, keep[-1] + 1):
+        q = imexcore.ark_imex_step(q, dt, tab, prob, rhs)
+        if k in keep:
+            e_rho, e_vel, e_th = rel_fields(o.to_lattice(q.cpu().numpy()), g[f"step_q{k}"])
+            assert e_rho < STEP_SCALAR_TOL and e_th < STEP_SCALAR_TOL, (name, k, e_rho, e_th)
+            assert e_vel < STEP_VEL_TOL, (name, k, e_vel)
+    assert prob.stats.solves == 2 * keep[-1]
+    assert prob.lam == pytest.approx(tab.diag * dt)
+
+
+def test_dt_rule_matches_reference(case):
+    from paper_1702_04316_b200 import cases
+    name, mesh, ref, disc, o, g = case
+    q = dev(g["step_q0"])
+    dt = cases.dt_for_courant(mesh, ref, q, CASES[name]["courant"])
+    assert dt == pytest.approx(float(g["step_dt"]), rel=1e-13)
+
+
+def test_fused_step_equals_generic_stage_loop(case):
+    """The fused 5-kernel schedule and the reference stage loop over the
+    individual device operators agree (same kernels, different glue)."""
+    name, mesh, ref, disc, o, g = case
+    q = dev(o.from_lattice(g["step_q0"]))
+    dt = float(g["step_dt"])
+    tab = imexcore.ark2_tableau()
+    p1 = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                  solver=imexcore.SolverSpec(method="direct"))
+    p2 = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                  solver=imexcore.SolverSpec(method="direct"))
+    fused = imexcore.ark_imex_step(q, dt, tab, p1, euler.make_rhs(ref, disc, "set2nc"))
+    generic = imexcore.ark_imex_step(q, dt, tab, p2,
+                                     lambda s: euler.nonlinear_rhs(s, ref, disc, "set2nc"))
+    errs = rel_fields(fused.cpu().numpy(), generic.cpu().numpy())
+    assert max(errs) < 1e-13, errs
+    assert p1.stats.solves == p2.stats.solves == 2
+
+
+def test_step_is_bitwise_deterministic(case):
+    name, mesh, ref, disc, o, g = case
+    q = dev(o.from_lattice(g["step_q0"]))
+    dt = float(g["step_dt"])
+    tab = imexcore.ark2_tableau()
+    outs = []
+    for _ in range(2):
+        prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                        solver=imexcore.SolverSpec(method="direct"))
+        r = q
+        for _ in range(3):
+            r = imexcore.ark_imex_step(r, dt, tab, prob, euler.make_rhs(ref, disc, "set2nc"))
+        outs.append(r.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_oracle_agrees_with_gpu_on_fresh_random_state(case):
+    """GPU vs the CPU oracle on an input that is not in the fixtures."""
+    name, mesh, ref, disc, o, g = case
+    rng = np.random.default_rng(123)
+    ql = 1e-3 * rng.standard_normal(g["ops_q"].shape) * np.array(
+        [ref.rho0.mean(), 1, 1, 1, 300.0])[:, None, None, None]
+    if mesh.slab:
+        ql[..., 1, :] = ql[..., 0, :]
+        ql[2] = 0.0
+    q = o.from_lattice(ql)
+    R = euler.nonlinear_rhs(dev(q), ref, disc, "set2nc").cpu().numpy()
+    e_rho, e_vel, e_th = rel_fields(o.to_lattice(R), o.to_lattice(o.rhs(q)))
+    assert e_rho < OPS_SCALAR_TOL and e_th < OPS_SCALAR_TOL and e_vel < OPS_MOM_TOL
+    lam = 0.37
+    prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                    solver=imexcore.SolverSpec(method="direct"), lam=lam)
+    S = prob.solve(dev(q)).cpu().numpy()
+    assert max(rel_fields(o.to_lattice(S), o.to_lattice(o.solve(q, lam)))) < SOLVE_TOL
