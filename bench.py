@@ -1,0 +1,464 @@
+"""Benchmark of the B200 HEVI 1D-IMEX ARK2 step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
+    python bench.py --impl reference ...     # the reference CPU path (oracle port)
+
+One "step" is one ARK2 HEVI time step (3 explicit evaluations, 2 Schur
+column solves) of the whole grid.  ``value`` = unique DOF-updates/s with the
+state resident in HBM (5 fields x unique lattice points / step time, whole
+job, max over ranks); ``e2e`` = the same metric through the reference-facing
+call ``imexcore.ark_imex_step`` on host (pinned) E-vector buffers, H2D + D2H
+inside the timed region.  Default workload: SURVEY 8(d) config 5 (the
+largest single-GPU configuration), C = 15.  For N > 1 (torchrun) the same
+grid is split into px x py column blocks with NCCL halo exchange (strong
+scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DOF-updates/s (fp64) per 1D-IMEX step at C=15, 1/2/4/8 B200; % HBM roofline"
+UNIT = "DOF-updates/s"
+
+# SURVEY 8(d) configurations (3D box, 40:1 elements, neutral 300 K background)
+CONFIGS = {
+    "cfg5": dict(nx=176, ny=176, nz=10, N=4, Lx=704_000.0, Ly=704_000.0, Lz=1000.0,
+                 centre=(352_000.0, 352_000.0, 350.0), radii=(10_000.0, 10_000.0, 250.0),
+                 courant=15.0,
+                 desc="cfg5: 3D rising thermal bubble, 176x176x10 elements N=4 "
+                      "(704x704x1 km, 4 km x 100 m elements), HEVI ARK2 Schur direct, C=15"),
+    "cfg1": dict(nx=10, ny=10, nz=10, N=4, Lx=40_000.0, Ly=40_000.0, Lz=1000.0,
+                 centre=(20_000.0, 20_000.0, 350.0), radii=(250.0, 250.0, 250.0),
+                 courant=15.0,
+                 desc="cfg1: 3D rising thermal bubble, 10x10x10 elements N=4 (40x40x1 km), C=15"),
+}
+
+# algorithmic HBM bytes per unique point, per launch: each field
+# read / written once; 8 B per fp64 value
+KERNEL_BYTES_PER_POINT = {
+    "explicit_stage0": 8 * (5 + 15),
+    "solve_stage0": 8 * (3 + 3),
+    "explicit_stage1": 8 * (15 + 10),
+    "solve_stage1": 8 * (3 + 3),
+    "explicit_stage2": 8 * (10 + 5),
+}
+STEP_BYTES_PER_POINT = sum(KERNEL_BYTES_PER_POINT.values())   # 576 B
+SURVEY_BYTES_PER_POINT = 640                                   # SURVEY 8(d) 16 state passes
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port of the reference algorithm
+# ---------------------------------------------------------------------------
+
+def reference_sample(steps, warmup, budget_s=150.0, cfg_name="cfg5"):
+    """Time the CPU port on a bounded sample of the workload: an n x n x nz
+    sub-box with the same elements (4 km x 4 km x 100 m, N=4) and bubble
+    shape, n sized so (steps + warmup) steps fit the time budget."""
+    import numpy as np
+    from oracle.hevi_oracle import BoxOracle
+    cfg = CONFIGS[cfg_name]
+    ex = cfg["Lx"] / cfg["nx"]
+    ez = cfg["Lz"] / cfg["nz"]
+    n = int(20 * math.sqrt(budget_s / (1.7 * max(1, steps + warmup))))
+    n = max(4, min(20, n, cfg["nx"]))
+    o = BoxOracle(n, n, cfg["nz"], n * ex, n * ex, cfg["nz"] * ez, cfg["N"])
+    q = o.bubble(0.5, (0.5 * n * ex, 0.5 * n * ex, cfg["centre"][2]), cfg["radii"])
+    dt = o.dt_for_courant(q, cfg["courant"])
+    for _ in range(max(1, warmup)):
+        q = o.step(q, dt)          # first step also probes + factors the columns
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        q = o.step(q, dt)
+        times.append(time.perf_counter() - t0)
+    med = float(np.median(times))
+    n_unique = o.X * o.Y * o.Z
+    return {"value": 5 * n_unique / med, "ms_per_step": 1e3 * med, "n": n,
+            "sample": f"{n}x{n}x{cfg['nz']} elements N={cfg['N']} sub-box of {cfg_name} "
+                      f"({n_unique} unique points), median of {len(times)} oracle steps "
+                      f"after {max(1, warmup)} warm-up (factor) step(s)",
+            "storage_dof_per_s": 5 * o.nel * (o.N + 1) ** 3 / med}
+
+
+def cpu_threads():
+    return os.cpu_count() or 1
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cpu_threads()))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
+    r = reference_sample(args.steps, args.warmup, cfg_name=args.config)
+    cfg = CONFIGS[args.config]
+    out = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg["desc"], "sample": r["sample"],
+                      "parallelism": "single host process (numpy)"},
+           "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": cpu_threads(),
+                            "kind": "port", "sample": r["sample"],
+                            "note": "oracle/hevi_oracle.py (numpy restatement of dycore); "
+                                    "OpenBLAS threads allowed, the 5x5 dgemms do not thread"},
+           "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1702_04316_b200 import specgrid, euler, imexcore, cases
+    from paper_1702_04316_b200.plan import tableau_array
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    mesh = specgrid.build_box_mesh_3d(cfg["nx"], cfg["ny"], cfg["nz"], cfg["Lx"], cfg["Ly"],
+                                      cfg["Lz"], cfg["N"])
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    q0 = cases.bubble_lattice(mesh, ref, 0.5, cfg["centre"], cfg["radii"])
+    dt = cases.dt_for_courant(mesh, ref, q0, cfg["courant"])
+    tab = imexcore.ark2_tableau()
+    lam = tab.diag * dt
+    n_unique = mesh.n_unique
+    dof = 5 * n_unique
+
+    if world == 1:
+        plan = disc.plan_for(ref)
+        plan.factor(lam)
+        Q = plan.zeros()
+        Q[..., :mesh.X].copy_(q0)
+        work = plan.workspace()
+        exch = None
+        px, py = 1, 1
+    else:
+        from paper_1702_04316_b200.distributed import DistributedStepper, grid_for
+        px, py = grid_for(world)
+        ds = DistributedStepper(mesh, ref, disc, dt, px, py, rank)
+        ds.load_global(q0)
+        plan, Q, work, exch = ds.plan, ds.Q, ds.work, ds.exchange
+    del q0
+    tarr = tableau_array(tab)
+    stream = torch.cuda.current_stream()
+    names = list(KERNEL_BYTES_PER_POINT)
+
+    def one_step(ev=None):
+        if exch is not None:
+            exch(Q)
+        if ev is not None:
+            ev[0].record(stream)
+        plan.stage(0, dt, tarr, Q, work)
+        if ev is not None:
+            ev[1].record(stream)
+        plan.stage_solve(0, lam, work)
+        if ev is not None:
+            ev[2].record(stream)
+        if exch is not None:
+            exch(work[0])
+            if ev is not None:
+                ev[6].record(stream)
+        else:
+            if ev is not None:
+                ev[6] = ev[2]
+        plan.stage(1, dt, tarr, Q, work)
+        if ev is not None:
+            ev[3].record(stream)
+        plan.stage_solve(1, lam, work)
+        if ev is not None:
+            ev[4].record(stream)
+        if exch is not None:
+            exch(work[1])
+            if ev is not None:
+                ev[7].record(stream)
+        else:
+            if ev is not None:
+                ev[7] = ev[4]
+        plan.stage(2, dt, tarr, Q, work)
+        if ev is not None:
+            ev[5].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    plan.check_flags()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for k in range(args.steps):
+        one_step(evs[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    elapsed = t_start.elapsed_time(t_end)    # ms
+    ktimes = {n: 0.0 for n in names}
+    for ev in evs:
+        ktimes["explicit_stage0"] += ev[0].elapsed_time(ev[1])
+        ktimes["solve_stage0"] += ev[1].elapsed_time(ev[2])
+        ktimes["explicit_stage1"] += ev[6].elapsed_time(ev[3])
+        ktimes["solve_stage1"] += ev[3].elapsed_time(ev[4])
+        ktimes["explicit_stage2"] += ev[7].elapsed_time(ev[5])
+    plan.check_flags()
+    if world > 1:
+        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        kt = torch.tensor([ktimes[n] for n in names], device="cuda", dtype=torch.float64)
+        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+        ktimes = {n: float(v) for n, v in zip(names, kt.tolist())}
+    ms_step = elapsed / args.steps
+    value = dof / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (per rank: points this rank owns)
+    pts_rank = n_unique / world
+    peak, peak_src = peaks()
+    kern = {}
+    for n in names:
+        avg = ktimes[n] / args.steps
+        gbs = KERNEL_BYTES_PER_POINT[n] * pts_rank / (avg * 1e-3) / 1e9
+        kern[n] = {"ms": round(avg, 4), "alg_bytes_per_point": KERNEL_BYTES_PER_POINT[n],
+                   "alg_GBps": round(gbs, 1), "share": round(ktimes[n] / elapsed, 4)}
+    dom = max(names, key=lambda n: ktimes[n])
+    traffic = None
+    summ = ncu_traffic()
+    if summ and args.config in summ and dom in summ[args.config]:
+        traffic = summ[args.config][dom].get("dram_bytes_per_launch")
+    achieved = kern[dom]["alg_GBps"]
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "alg_bytes_per_launch": KERNEL_BYTES_PER_POINT[dom] * pts_rank,
+            "peak_source": peak_src}
+    step_gbs = STEP_BYTES_PER_POINT * pts_rank / (ms_step * 1e-3) / 1e9
+    step_roof = {"alg_bytes_per_point": STEP_BYTES_PER_POINT, "achieved_GBps": round(step_gbs, 1),
+                 "frac": round(step_gbs / peak, 4),
+                 "survey_640B_frac": round(SURVEY_BYTES_PER_POINT * pts_rank / (ms_step * 1e-3)
+                                           / 1e9 / peak, 4)}
+
+    # e2e through the reference-facing call with host buffers (rank 0 drives
+    # the single-GPU drop-in; N > 1 ranks do window H2D / owned D2H)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, mesh, ref, disc, dt, tab, plan, Q, work, exch, world, rank, dof)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = reference_sample(args.cpu_steps, 1, budget_s=args.cpu_budget, cfg_name=args.config)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": r["sample"], "ms_per_step": r["ms_per_step"]}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic",
+               "config": {"workload": cfg["desc"], "unique_points": n_unique,
+                          "unique_dof": dof, "storage_dof": 5 * mesh.n_nodes,
+                          "columns": mesh.n_col, "levels": mesh.n_lev, "dt_s": dt,
+                          "parallelism": f"columns {px}x{py}",
+                          "l2": "inputs larger than L2 (state %.0f MB vs 126 MB L2)"
+                                % (8 * dof / 1e6)},
+               "storage_dof_per_s": 5 * mesh.n_nodes / (ms_step * 1e-3),
+               "roofline": roof, "step_roofline": step_roof, "kernels": kern,
+               "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+               "gpu_launches": 5 * args.steps * 1}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, mesh, ref, disc, dt, tab, plan, Q, work, exch, world, rank, dof):
+    import torch
+    from paper_1702_04316_b200 import imexcore, euler
+    from paper_1702_04316_b200.plan import tableau_array
+    if world == 1:
+        prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                        solver=imexcore.SolverSpec(method="direct"))
+        rhs = euler.make_rhs(ref, disc, "set2nc")
+        host = torch.empty((5,) + tuple(mesh.nshape), dtype=torch.float64, pin_memory=True)
+        host.copy_(plan.l2e(Q))
+        torch.cuda.synchronize()
+        q = imexcore.ark_imex_step(host, dt, tab, prob, rhs)      # warm (pinned pools)
+        times = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            q = imexcore.ark_imex_step(q, dt, tab, prob, rhs)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        ms = 1e3 * sorted(times)[len(times) // 2]
+        nbytes = host.numel() * 8
+        return {"value": dof / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                "d2h_bytes_per_step": nbytes, "ms_per_step": ms,
+                "path": "imexcore.ark_imex_step(pinned host E-vector) -> H2D, E->lattice, "
+                        "fused step, lattice->E, D2H"}
+    # multi-GPU: the rank's window in, its owned block out, per step
+    import torch.distributed as dist
+    tarr = tableau_array(tab)
+    lam = tab.diag * dt
+    hin = torch.empty_like(Q, device="cpu").pin_memory()
+    hout = torch.empty_like(Q, device="cpu").pin_memory()
+    hin.copy_(Q)
+    times = []
+    for _ in range(args.e2e_steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Q.copy_(hin, non_blocking=True)
+        exch(Q)
+        plan.stage(0, dt, tarr, Q, work)
+        plan.stage_solve(0, lam, work)
+        exch(work[0])
+        plan.stage(1, dt, tarr, Q, work)
+        plan.stage_solve(1, lam, work)
+        exch(work[1])
+        plan.stage(2, dt, tarr, Q, work)
+        hout.copy_(Q, non_blocking=True)
+        torch.cuda.synchronize()
+        plan.check_flags()
+        t = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t.item()))
+    ms = 1e3 * sorted(times)[len(times) // 2]
+    nbytes = Q.numel() * 8
+    return {"value": dof / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes * world,
+            "d2h_bytes_per_step": nbytes * world, "ms_per_step": ms,
+            "path": "per-rank pinned window H2D, partitioned fused step, D2H"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=4)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

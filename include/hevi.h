@@ -60,6 +60,9 @@ typedef struct {
 typedef struct {
     const double *rho0, *theta0, *P0f, *drho0, *dtheta0;
     const double *G0, *H0, *F0z, *rho0G0;
+    const double *Pb;       /* EOS(rho0, theta0) per level: euler.equation_of_state
+                               of the background, the reference point of the
+                               P' = P - P0f evaluation (euler.py:454-457)      */
     const double *cx, *cy, *cz;
     const double *Dx, *Dy, *Dz;
     double g, R, P0, gamma;

@@ -1,0 +1,560 @@
+// explicit_v2.cuh -- production explicit-stage kernel (included by hevi.cu
+// inside its anonymous namespace).
+//
+// One CTA per horizontal tile of TX x TY element columns sweeps the element
+// layers bottom-up.  Per layer:
+//   1. TMA (cp.async.bulk.tensor, 4D box x,y,z,field) brings the layer's
+//      N+1 levels of the 5 input fields for the tile plus its low-side halo
+//      into a staging buffer; the load of layer ez+1 is issued right after
+//      layer ez has been converted, so it runs underneath layer ez's compute;
+//   2. the staged levels are converted into a ring buffer of N+1 level slots
+//      (the top level of a layer is the bottom of the next): the 5 fields,
+//      P' and the linearised pressure.  P' = EOS(rho, theta) - P0f
+//      (euler.py:454-457) is evaluated as Pb (1+delta)^gamma - P0f with
+//      delta = (rho theta - rho0 theta0)/(rho0 theta0) by its binomial series
+//      (15 terms, |delta| <= 1/8; exact pow beyond): the same function,
+//      ~20 FMAs instead of a ~240-instruction pow, and no cancellation;
+//   3. per-layer partial sums that more than one point needs are formed once:
+//      row N of the left element at element x-faces, row N of this layer at
+//      its top face (the carry into the next layer's bottom face);
+//   4. one thread per owned lattice point: 19 derivative lines with the
+//      thread's D rows held in registers for the whole sweep, R(q) and
+//      L_V(q) pointwise, no-flux projection, fused ARK2 stage epilogue.
+#pragma once
+
+template <int N, int NY, int TX, int TY>
+struct E2 {
+    static constexpr int OX = TX * N;                         // main x points per tile
+    static constexpr int OYM = TY * NY + (NY == 1 ? 1 : 0);   // main y rows (slab: both)
+    static constexpr int LX = OX + N + 1;                     // loaded x extent (low halo N)
+    // TMA box x: 16-byte multiple and one spare column, because the box
+    // x-origin is floored to an even index (an odd, negative origin is an
+    // illegal TMA request on sm_100a; tools/tma_probe.cu)
+    static constexpr int LXT = (LX + 2) / 2 * 2;
+    static constexpr int LY = TY * NY + NY + 1;
+    static constexpr int NL = N + 1;                          // level slots (ring)
+    static constexpr int PL = LY * LXT;                       // one level plane
+    static constexpr int NT = OX * OYM * N;                   // main points == threads
+    static constexpr int BLK = (NT + 31) / 32 * 32;
+    static constexpr int CXW = OX + 1, CYW = TY * NY + 1 + (NY == 1 ? 1 : 0);
+    static constexpr int STG_N = 5 * NL * PL;                 // TMA staging
+    static constexpr int S_N = 7 * NL * PL;                   // ring of 7 fields
+    static constexpr int CAR_N = 2 * 7 * CYW * CXW;           // double-buffered carry
+    static constexpr int XF_N = 6 * TX * OYM * N;             // x-face partials
+    static constexpr int DN = (N + 1) * (N + 1), DNY = (NY + 1) * (NY + 1);
+    static constexpr size_t fixed_bytes() {
+        return sizeof(double) * (size_t)(STG_N + S_N + CAR_N + XF_N + DN + DNY + 1) + 128;
+    }
+    static constexpr int NTAB = 12;                           // level tables in smem
+    static constexpr uint32_t TMA_BYTES = (uint32_t)(sizeof(double) * STG_N);
+};
+
+// smem level tables
+enum { T_RHO0 = 0, T_TH0, T_E0, T_C0, T_IRT0, T_G0, T_H0, T_DRHO0, T_DTH0, T_CZ, T_P0F, T_IRHO0 };
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+// P' at one point; rho0/theta0/Pb/c0/irt0 of its level
+__device__ __forceinline__ double pprime(double r, double th, double rho0, double th0, double Pb,
+                                         double c0, double irt0, double P0f, const double* bc,
+                                         const Phys& ph) {
+    const double delta = (r * th0 + th * (rho0 + r)) * irt0;
+    if (fabs(delta) <= 0.125) {
+        double s = bc[14];
+#pragma unroll
+        for (int k = 13; k >= 0; --k) s = fma(s, delta, bc[k]);
+        return fma(Pb, s * delta, c0);
+    }
+    const double rho = rho0 + r, theta = th0 + th;
+    return ph.P0 * pow(rho * ph.R * theta / ph.P0, ph.gamma) - P0f;
+}
+
+template <int N, int NY>
+struct DRows {
+    double x[N + 1], y[NY + 1], z[N + 1];   // the point's own rows; face rows (row N) from smem
+};
+
+// per-axis geometry of one point inside the tile
+struct PAx {
+    int l, s0, row;
+    bool face;
+};
+
+__device__ __forceinline__ PAx pax(int gi, int l, int N, int ne) {
+    PAx r;
+    r.l = l;
+    if (gi == ne * N) {
+        r.row = N;
+        r.s0 = l - N;
+        r.face = false;
+    } else {
+        r.row = gi % N;
+        r.s0 = l - r.row;
+        r.face = (r.row == 0) && (gi > 0);
+    }
+    return r;
+}
+
+template <int N, int NY, int TX, int TY, int MODE, bool MAIN>
+__device__ __forceinline__ void e2_point(const EArgs& a, const double* __restrict__ S,
+                                         const double* __restrict__ CARp,
+                                         const double* __restrict__ XF, const double* __restrict__ LT,
+                                         const DRows<N, NY>& D, const double* __restrict__ sDx,
+                                         const double* __restrict__ sDy, const PAx& ax, const PAx& ay,
+                                         int oz, int ox, int oy, int gx, int gy, int gz, int ez,
+                                         double cx, double cy, int Z) {
+    using T = E2<N, NY, TX, TY>;
+    constexpr int PL = T::PL, LXT = T::LXT, NL = T::NL;
+    constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
+    constexpr bool NEED_R = (MODE != M_L);
+    const Geo& g = a.g;
+    const long long o = loff(g, gx, gy, gz);
+    const long long fs = g.fs;
+    // stage inputs read pointwise: issue early, consume in the epilogue
+    double Ain[5], Fin[5];
+    if (MODE == M_S2) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) Ain[f] = a.A[o + f * fs];
+    }
+    if (MODE == M_S2 || MODE == M_S3) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) Fin[f] = a.F[o + f * fs];
+    }
+    const int base = ez * N;
+    const int sl = (base + oz) % NL;
+    int zs[N + 1];
+#pragma unroll
+    for (int m = 0; m <= N; ++m) zs[m] = ((base + m) % NL) * PL;
+    const double cz = LT[T_CZ * Z + gz];
+    const int cidx = oy * T::CXW + ox;
+    const int pnt = sl * PL + ay.l * LXT + ax.l;
+
+    // pointwise values first: every derivative is folded into the
+    // accumulators as soon as it is formed (R is affine in the gradients)
+    const double r = S[0 * NL * PL + pnt], u = S[1 * NL * PL + pnt], v = S[2 * NL * PL + pnt],
+                 w = S[3 * NL * PL + pnt], th = S[4 * NL * PL + pnt];
+    const double rho0 = LT[T_RHO0 * Z + gz];
+    const double rho = rho0 + r;
+    const double rinv = 1.0 / rho;
+    const double gr = a.ph.g;
+    // one field's (d/dx, d/dy, d/dz) at the point, DSS-averaged (folded)
+    auto grad = [&](int f, double& gx_, double& gy_, double& gz_, bool want_xy) {
+        const double* Sf = S + f * (NL * PL);
+        if (want_xy) {
+            const double* sx = Sf + sl * PL + ay.l * LXT + ax.s0;
+            double d = 0.0;
+#pragma unroll
+            for (int m = 0; m <= N; ++m) d = fma(D.x[m], sx[m], d);
+            if (ax.face) {
+                if (MAIN) {
+                    d += XF[((f * TX + ox / N) * T::OYM + oy) * N + oz];
+                } else {
+                    const double* sxl = Sf + sl * PL + ay.l * LXT + ax.l - N;
+                    double e = 0.0;
+#pragma unroll
+                    for (int m = 0; m <= N; ++m) e = fma(sDx[N * (N + 1) + m], sxl[m], e);
+                    d += e;
+                }
+            }
+            gx_ = cx * d;
+            const double* sy = Sf + sl * PL + ay.s0 * LXT + ax.l;
+            double e = 0.0;
+#pragma unroll
+            for (int m = 0; m <= NY; ++m) e = fma(D.y[m], sy[m * LXT], e);
+            if (ay.face) {
+                const double* syl = Sf + sl * PL + (ay.l - NY) * LXT + ax.l;
+                double h = 0.0;
+#pragma unroll
+                for (int m = 0; m <= NY; ++m) h = fma(sDy[NY * (NY + 1) + m], syl[m * LXT], h);
+                e += h;
+            }
+            gy_ = cy * e;
+        }
+        const double* sz = Sf + ay.l * LXT + ax.l;
+        double d = 0.0;
+#pragma unroll
+        for (int m = 0; m <= N; ++m) d = fma(D.z[m], sz[zs[m]], d);
+        if (oz == 0 && ez > 0) d += CARp[f * (T::CYW * T::CXW) + cidx];
+        gz_ = cz * d;
+    };
+    double R0 = 0.0, R1 = 0.0, R2 = 0.0, R3 = 0.0, R4 = 0.0;
+    double dwz = 0.0, dPLz = 0.0;
+    {
+        double gxv, gyv, gzv;
+        double divu;
+        if (NEED_R) {
+            grad(0, gxv, gyv, gzv, true);
+            R0 = (u * gxv + v * gyv) + w * gzv;                       // u . grad rho'
+            grad(1, gxv, gyv, gzv, true);
+            R1 = (u * gxv + v * gyv) + w * gzv;
+            divu = gxv;
+            grad(2, gxv, gyv, gzv, true);
+            R2 = (u * gxv + v * gyv) + w * gzv;
+            divu += gyv;
+        }
+        grad(3, gxv, gyv, gzv, NEED_R);
+        dwz = gzv;
+        if (NEED_R) {
+            R3 = (u * gxv + v * gyv) + w * gzv;
+            divu += gzv;
+            grad(4, gxv, gyv, gzv, true);
+            R4 = (u * gxv + v * gyv) + w * gzv;
+            grad(5, gxv, gyv, gzv, true);                              // grad P'
+            R1 += gxv * rinv;
+            R2 += gyv * rinv;
+            R3 += gzv * rinv;
+            R0 += rho * divu;
+        }
+        if (NEED_L) {
+            double dummy_x = 0.0, dummy_y = 0.0;
+            grad(6, dummy_x, dummy_y, gzv, false);                      // d/dz of linearised P
+            dPLz = gzv;
+        }
+    }
+    const double drho0 = LT[T_DRHO0 * Z + gz];
+    const double dth0 = LT[T_DTH0 * Z + gz];
+    const bool bx = (gx == 0) || (gx == g.X - 1);
+    const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
+    const bool bz = (gz == 0) || (gz == g.Z - 1);
+    if (NEED_R) {
+        const double theta = LT[T_TH0 * Z + gz] + th;
+        if (!(isfinite(r) && isfinite(u) && isfinite(v) && isfinite(w) && isfinite(th)))
+            atomicOr(a.flags, HEVI_F_NONFINITE_IN(a.stage));
+        if (!(rho > 0.0) || !(theta > 0.0)) atomicOr(a.flags, HEVI_F_EOS(a.stage));
+        // euler.nonlinear_rhs set2nc (euler.py:458-473), DSS folded into the derivatives
+        R0 = -(R0 + w * drho0);
+        R1 = -R1;
+        R2 = -R2;
+        R3 = -(R3 + (r * rinv) * gr);
+        R4 = -(R4 + w * dth0);
+        if (bx) R1 = 0.0;
+        if (by) R2 = 0.0;
+        if (bz) R3 = 0.0;
+    }
+    double L0 = 0.0, L3 = 0.0, L4 = 0.0;
+    if (NEED_L) {
+        // euler.linear_operator(vertical_only=True), set2nc (euler.py:333-361)
+        const double irho0 = LT[T_IRHO0 * Z + gz];
+        L0 = -(w * drho0 + rho0 * dwz);
+        L3 = bz ? 0.0 : -(dPLz * irho0 + (r * irho0) * gr);
+        L4 = -(w * dth0);
+    }
+    if (MODE == M_R) {
+        a.out[o] = R0;
+        a.out[o + fs] = R1;
+        a.out[o + 2 * fs] = R2;
+        a.out[o + 3 * fs] = R3;
+        a.out[o + 4 * fs] = R4;
+    } else if (MODE == M_L) {
+        a.out[o] = L0;
+        a.out[o + fs] = 0.0;
+        a.out[o + 2 * fs] = 0.0;
+        a.out[o + 3 * fs] = L3;
+        a.out[o + 4 * fs] = L4;
+    } else if (MODE == M_S1) {
+        // imexcore.ark_imex_step (imexcore.py:398-403, 409-411)
+        const double dt = a.dt;
+        const double qv[5] = {r, u, v, w, th};
+        const double Rv[5] = {R0, R1, R2, R3, R4};
+        const double Lv[5] = {L0, 0.0, 0.0, L3, L4};
+        double pr[5];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            pr[f] = qv[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+            a.A[o + f * fs] = qv[f] + dt * (a.a_a * (Rv[f] - Lv[f]) + a.at_a * Lv[f]);
+            a.F[o + f * fs] = qv[f] + a.cb * Rv[f];
+        }
+        a.P[o] = pr[0];
+        a.P[o + 3 * fs] = pr[3];
+        a.P[o + 4 * fs] = pr[4];
+        a.Quv[o + fs] = bx ? 0.0 : pr[1];
+        a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+    } else if (MODE == M_S2) {
+        const double dt = a.dt;
+        const double Rv[5] = {R0, R1, R2, R3, R4};
+        const double Lv[5] = {L0, 0.0, 0.0, L3, L4};
+        double pr[5];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            pr[f] = Ain[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+            a.F[o + f * fs] = Fin[f] + a.cb * Rv[f];
+        }
+        a.P[o] = pr[0];
+        a.P[o + 3 * fs] = pr[3];
+        a.P[o + 4 * fs] = pr[4];
+        a.Quv[o + fs] = bx ? 0.0 : pr[1];
+        a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+    } else {
+        const double Rv[5] = {R0, R1, R2, R3, R4};
+        bool fin = true;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            const double val = Fin[f] + a.cb * Rv[f];
+            fin = fin && isfinite(val);
+            a.out[o + f * fs] = val;
+        }
+        if (!fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
+    }
+}
+
+template <int N, int NY, int TX, int TY>
+__device__ __forceinline__ void stage_manual(double* STG, const EArgs& a, int tx0, int ty0, int z0) {
+    using T = E2<N, NY, TX, TY>;
+    const Geo& g = a.g;
+    constexpr int TOT = 5 * T::NL * T::LY * T::LXT;
+    for (int i = threadIdx.x; i < TOT; i += T::BLK) {
+        const int x = i % T::LXT;
+        int t = i / T::LXT;
+        const int y = t % T::LY;
+        t /= T::LY;
+        const int z = t % T::NL;
+        const int f = t / T::NL;
+        const int ix = tx0 + x, iy = ty0 + y, iz = z0 + z;
+        double v = 0.0;
+        if (ix >= 0 && ix < g.lX && iy >= 0 && iy < g.lY && iz < g.Z)
+            v = a.q[f * g.fs + ((long long)iz * g.lY + iy) * g.px + ix];
+        STG[i] = v;
+    }
+}
+
+template <int N, int NY, int TX, int TY, int MODE>
+__global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, 1)
+    k_explicit2(const EArgs a, const __grid_constant__ CUtensorMap tmap) {
+    using T = E2<N, NY, TX, TY>;
+    constexpr int PL = T::PL, LXT = T::LXT, NL = T::NL, BLK = T::BLK;
+    constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
+    constexpr bool NEED_R = (MODE != M_L);
+    extern __shared__ __align__(128) unsigned char smraw[];
+    // TMA destinations must be 128-byte aligned: align the carve-up explicitly
+    double* smd = reinterpret_cast<double*>(
+        smraw + ((128u - ((unsigned)__cvta_generic_to_shared(smraw) & 127u)) & 127u));
+    double* STG = smd;
+    double* S = STG + T::STG_N;
+    double* CAR = S + T::S_N;
+    double* XF = CAR + T::CAR_N;
+    double* sDx = XF + T::XF_N;
+    double* sDy = sDx + T::DN;
+    double* LT = sDy + T::DNY;
+    uint64_t* mbarp = reinterpret_cast<uint64_t*>(LT + T::NTAB * a.g.Z);
+    uint64_t& mbar = *mbarp;
+    const Geo& g = a.g;
+    const int Z = g.Z;
+    const int tid = threadIdx.x;
+    const int ex0 = g.ex_b + blockIdx.x * TX;
+    const int ey0 = g.ey_b + blockIdx.y * TY;
+    const int nxe = min(TX, g.ex_e - ex0);
+    const int nye = min(TY, g.ey_e - ey0);
+    const int oxn = nxe * N + ((ex0 + nxe == g.nex) ? 1 : 0);
+    const int oyn = nye * NY + ((ey0 + nye == g.ney) ? 1 : 0);
+    const int oxm = nxe * N;                                  // main x extent
+    const int oym = nye * NY + (NY == 1 ? 1 : 0);             // main y extent
+    const int gxlo = (ex0 - 1) * N, gylo = (ey0 - 1) * NY;
+
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+    }
+    for (int i = tid; i < T::DN; i += BLK) sDx[i] = a.Dx[i];
+    for (int i = tid; i < T::DNY; i += BLK) sDy[i] = a.Dy[i];
+    for (int k = tid; k < Z; k += BLK) {
+        LT[T_RHO0 * Z + k] = a.lv.rho0[k];
+        LT[T_TH0 * Z + k] = a.lv.theta0[k];
+        LT[T_E0 * Z + k] = a.lv.E0[k];
+        LT[T_C0 * Z + k] = a.lv.c0[k];
+        LT[T_IRT0 * Z + k] = a.lv.irt0[k];
+        LT[T_G0 * Z + k] = a.lv.G0[k];
+        LT[T_H0 * Z + k] = a.lv.H0[k];
+        LT[T_DRHO0 * Z + k] = a.lv.drho0[k];
+        LT[T_DTH0 * Z + k] = a.lv.dth0[k];
+        LT[T_CZ * Z + k] = a.cz[k];
+        LT[T_P0F * Z + k] = a.lv.P0f[k];
+        LT[T_IRHO0 * Z + k] = 1.0 / a.lv.rho0[k];
+    }
+    __syncthreads();
+    // window-local TMA coordinates of the tile origin
+    const int txr = gxlo - g.x0, ty0 = gylo - g.y0;
+    const int xsh = txr & 1;          // staged column of lx is lx + xsh
+    const int tx0 = txr - xsh;
+    const bool use_tma = a.use_tma != 0;
+    if (use_tma) {
+        if (tid == 0) {
+            mbar_expect_tx(&mbar, T::TMA_BYTES);
+            tma_load_4d(STG, &tmap, &mbar, tx0, ty0, 0, 0);
+        }
+    } else {
+        stage_manual<N, NY, TX, TY>(STG, a, tx0, ty0, 0);
+        __syncthreads();
+    }
+
+    // ---- the thread's main point (fixed for the whole sweep) --------------
+    const bool has_main = tid < T::NT;
+    const int mox = tid % T::OX;
+    const int moz = (tid / T::OX) % N;
+    const int moy = tid / (T::OX * N);
+    const bool main_ok = has_main && mox < oxm && moy < oym;
+    const int mgx = ex0 * N + mox, mgy = ey0 * NY + moy;
+    const PAx max_ = pax(mgx, mox + N, N, g.nex);
+    const PAx may_ = pax(mgy, moy + NY, NY, g.ney);
+    DRows<N, NY> Dm;
+    double mcx = 0.0, mcy = 0.0;
+    if (main_ok) {
+#pragma unroll
+        for (int m = 0; m <= N; ++m) {
+            Dm.x[m] = sDx[max_.row * (N + 1) + m];
+            Dm.z[m] = sDx[moz * (N + 1) + m];
+        }
+#pragma unroll
+        for (int m = 0; m <= NY; ++m) Dm.y[m] = sDy[may_.row * (NY + 1) + m];
+        mcx = __ldg(a.cx + mgx);
+        mcy = __ldg(a.cy + mgy);
+    }
+    const double* bc = a.bc;
+
+    for (int ez = 0; ez < g.nez; ++ez) {
+        const int base = ez * N;
+        // ---------------- 1. staged layer -> ring slots ---------------------
+        if (use_tma) mbar_wait(&mbar, ez & 1);
+        const int lz0 = (ez == 0) ? 0 : 1;
+        const int nconv = (NL - lz0) * T::LY * T::LX;
+        for (int idx = tid; idx < nconv; idx += BLK) {
+            const int lx = idx % T::LX;
+            const int t = idx / T::LX;
+            const int ly = t % T::LY;
+            const int lz = lz0 + t / T::LY;
+            const int gz = base + lz;
+            const int st = (lz * T::LY + ly) * LXT + lx + xsh;
+            const double r = STG[0 * NL * PL + st], u = STG[1 * NL * PL + st],
+                         v = STG[2 * NL * PL + st], w = STG[3 * NL * PL + st],
+                         th = STG[4 * NL * PL + st];
+            double pp = 0.0, pl = 0.0;
+            if (NEED_R)
+                pp = pprime(r, th, LT[T_RHO0 * Z + gz], LT[T_TH0 * Z + gz], LT[T_E0 * Z + gz],
+                            LT[T_C0 * Z + gz], LT[T_IRT0 * Z + gz], LT[T_P0F * Z + gz], bc, a.ph);
+            if (NEED_L) pl = LT[T_G0 * Z + gz] * r + LT[T_H0 * Z + gz] * th;
+            const int d = ((gz % NL) * T::LY + ly) * LXT + lx;
+            S[0 * NL * PL + d] = r;
+            S[1 * NL * PL + d] = u;
+            S[2 * NL * PL + d] = v;
+            S[3 * NL * PL + d] = w;
+            S[4 * NL * PL + d] = th;
+            S[5 * NL * PL + d] = pp;
+            S[6 * NL * PL + d] = pl;
+        }
+        __syncthreads();
+        // the staging buffer is free: fetch the next layer under this layer's compute
+        if (use_tma) {
+            if (tid == 0 && ez + 1 < g.nez) {
+                // generic-proxy reads of STG are ordered before the async-proxy refill
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&mbar, T::TMA_BYTES);
+                tma_load_4d(STG, &tmap, &mbar, tx0, ty0, base + N, 0);
+            }
+        } else if (ez + 1 < g.nez) {
+            stage_manual<N, NY, TX, TY>(STG, a, tx0, ty0, base + N);
+            // (the barrier after the partial sums orders these writes before use)
+        }
+        // ---------------- 2. shared partial sums ----------------------------
+        double* CARw = CAR + (ez & 1) * (7 * T::CYW * T::CXW);
+        const double* CARr = CAR + ((ez + 1) & 1) * (7 * T::CYW * T::CXW);
+        {
+            // row N of the left element at the tile's element x-faces
+            constexpr int NXF = 6 * TX * T::OYM * N;
+            for (int it = tid; it < NXF; it += BLK) {
+                const int oz = it % N;
+                int t = it / N;
+                const int oy = t % T::OYM;
+                t /= T::OYM;
+                const int ae = t % TX;
+                const int f = t / TX;
+                const double* sx = S + f * (NL * PL) + ((base + oz) % NL) * PL + (oy + NY) * LXT + ae * N;
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sx[m], s);
+                XF[it] = s;
+            }
+            // row N of this layer at its top face: carry into the next layer
+            if (ez + 1 < g.nez) {
+                const int ncol = oxn * oyn;
+                for (int it = tid; it < 7 * ncol; it += BLK) {
+                    const int c = it % ncol;
+                    const int f = it / ncol;
+                    if ((f == 6 && !NEED_L) || (f == 5 && !NEED_R)) continue;
+                    const int ox = c % oxn, oy = c / oxn;
+                    const double* sz = S + f * (NL * PL) + (oy + NY) * LXT + (ox + N);
+                    double s = 0.0;
+#pragma unroll
+                    for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sz[((base + m) % NL) * PL], s);
+                    CARw[f * (T::CYW * T::CXW) + oy * T::CXW + ox] = s;
+                }
+            }
+        }
+        __syncthreads();
+        // ---------------- 3. points ------------------------------------------
+        if (main_ok) {
+            e2_point<N, NY, TX, TY, MODE, true>(a, S, CARr, XF, LT, Dm, sDx, sDy, max_, may_, moz,
+                                                mox, moy,
+                                                mgx, mgy, base + moz, ez, mcx, mcy, Z);
+        }
+        // points outside the main box: domain-end x column / y row, top level
+        const int ozn = N + ((ez == g.nez - 1) ? 1 : 0);
+        const int nfull = oxn * oyn * ozn;
+        if (nfull > oxm * oym * N) {
+            for (int p = tid; p < nfull; p += BLK) {
+                const int ox = p % oxn;
+                const int t = p / oxn;
+                const int oy = t % oyn;
+                const int oz = t / oyn;
+                if (ox < oxm && oy < oym && oz < N) continue;
+                const int gx = ex0 * N + ox, gy = ey0 * NY + oy, gz = base + oz;
+                const PAx ax = pax(gx, ox + N, N, g.nex);
+                const PAx ay = pax(gy, oy + NY, NY, g.ney);
+                const PAx az = pax(gz, oz, N, g.nez);
+                DRows<N, NY> De;
+#pragma unroll
+                for (int m = 0; m <= N; ++m) {
+                    De.x[m] = sDx[ax.row * (N + 1) + m];
+                    De.z[m] = sDx[az.row * (N + 1) + m];
+                }
+#pragma unroll
+                for (int m = 0; m <= NY; ++m) De.y[m] = sDy[ay.row * (NY + 1) + m];
+                e2_point<N, NY, TX, TY, MODE, false>(a, S, CARr, XF, LT, De, sDx, sDy, ax, ay, oz,
+                                                     ox, oy, gx,
+                                                     gy, gz, ez, __ldg(a.cx + gx), __ldg(a.cy + gy), Z);
+            }
+        }
+        __syncthreads();
+    }
+}

@@ -19,11 +19,13 @@
 //    (box meshes: all columns identical), extraction -- fused.
 #include "../../include/hevi.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -62,6 +64,7 @@ struct Geo {
 
 struct Lev {
     const double *rho0, *theta0, *P0f, *drho0, *dth0, *G0, *H0, *F0z, *rho0G0;
+    const double *E0, *c0, *irt0;   // EOS(rho0, theta0), E0 - P0f, 1/(rho0 theta0)
 };
 
 struct Phys {
@@ -85,6 +88,8 @@ struct EArgs {
     double dt, a_p, at_p, a_a, at_a, cb;
     unsigned* flags;
     int stage;
+    double bc[16];   // binomial coefficients C(gamma, k), k = 1..15 (EOS series)
+    int use_tma;     // 1: TMA staging (default); 0: cooperative loads
 };
 
 struct SArgs {
@@ -562,6 +567,7 @@ struct FArgs {
     const double* Dz;
     int N, nez, M, ainv_identity;
     double* lamtab;  // coefS | uA | den
+    double* vtab;    // 12 x M tables of the v2 column kernel
     double* A;       // M*M dense, row-major, zeroed
     unsigned* flags;
 };
@@ -578,6 +584,20 @@ __global__ void k_lamtab(const FArgs a) {
     a.lamtab[a.M + k] = uA;
     a.lamtab[2 * a.M + k] = den;
     if (!a.ainv_identity && fabs(den) < 1e-12) atomicOr(a.flags, HEVI_F_AINV);
+    const int M = a.M;
+    double* t = a.vtab;
+    t[0 * M + k] = a.lv.G0[k];
+    t[1 * M + k] = a.lv.H0[k];
+    t[2 * M + k] = a.lv.F0z[k];
+    t[3 * M + k] = a.lv.rho0G0[k];
+    t[4 * M + k] = a.cz[k];
+    t[5 * M + k] = a.lamtab[k];
+    t[6 * M + k] = uA;
+    t[7 * M + k] = den;
+    t[8 * M + k] = a.lv.dth0[k];
+    t[9 * M + k] = 1.0 / a.lv.rho0[k];
+    t[10 * M + k] = 1.0 / (a.lv.G0[k] * a.lv.rho0[k]);
+    t[11 * M + k] = 1.0 / a.lv.G0[k];
 }
 
 __device__ double f_unit(int l, int j) { return l == j ? 1.0 : 0.0; }
@@ -636,7 +656,7 @@ __global__ void k_probe(const FArgs a) {
 
 // single-CTA dense LU restricted to the band, band detection and packing
 __global__ void k_lu_dense(double* A, double* LU, double* LUb, int M, int* nb_out,
-                           unsigned* flags) {
+                           unsigned* flags, int N2, double* LU2, double* rU) {
     __shared__ double red[1024];
     __shared__ int redi[1024];
     __shared__ double s_norm;
@@ -691,6 +711,13 @@ __global__ void k_lu_dense(double* A, double* LU, double* LUb, int M, int* nb_ou
         const int j = k + d - (nb - 1);
         LUb[i] = (j >= 0 && j < M) ? LU[k * M + j] : 0.0;
     }
+    const int W2 = 4 * N2 + 1;
+    for (int i = tid; i < M * W2; i += T) {
+        const int k = i / W2, d = i % W2;
+        const int j = k + d - 2 * N2;
+        LU2[i] = (j >= 0 && j < M && abs(j - k) < nb) ? LU[k * M + j] : 0.0;
+    }
+    for (int k = tid; k < M; k += T) rU[k] = 1.0 / LU[k * M + k];
     if (tid == 0) *nb_out = nb;
 }
 
@@ -839,6 +866,9 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
     if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+#include "explicit_v2.cuh"
+#include "solve_v2.cuh"
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -851,6 +881,9 @@ struct Factor {
     double* LU = nullptr;      // M*M
     double* LUb = nullptr;     // M*(2*M-1) upper bound
     double* lamtab = nullptr;  // 3*M
+    double* vtab = nullptr;    // 12*M
+    double* LU2 = nullptr;     // M*(4N+1)
+    double* rU = nullptr;      // M
     int* d_nb = nullptr;
 };
 
@@ -864,6 +897,9 @@ struct hevi_plan {
     unsigned* d_flags = nullptr;
     unsigned* h_flags = nullptr;
     std::map<long long, Factor> factors;
+    double bc[16];
+    bool use_v2 = true;
+    bool use_tma = true;
 };
 
 namespace {
@@ -936,7 +972,133 @@ int dispatch_e(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     return fail("unsupported polynomial order (supported: N = 1..8; slab Ny = 1)");
 }
 
+// ---- v2 explicit dispatch (TMA ring-buffer kernel) ------------------------
+template <int N, int NY>
+struct Tile2 {
+    static constexpr int TX = 0, TY = 0;
+};
+template <> struct Tile2<1, 1> { static constexpr int TX = 16, TY = 16; };
+template <> struct Tile2<2, 2> { static constexpr int TX = 8, TY = 4; };
+template <> struct Tile2<3, 3> { static constexpr int TX = 4, TY = 2; };
+template <> struct Tile2<4, 4> { static constexpr int TX = 4, TY = 2; };
+template <> struct Tile2<5, 5> { static constexpr int TX = 2, TY = 2; };
+template <> struct Tile2<6, 6> { static constexpr int TX = 2, TY = 1; };
+template <> struct Tile2<7, 7> { static constexpr int TX = 1, TY = 1; };
+template <> struct Tile2<2, 1> { static constexpr int TX = 32, TY = 1; };
+template <> struct Tile2<3, 1> { static constexpr int TX = 16, TY = 1; };
+template <> struct Tile2<4, 1> { static constexpr int TX = 8, TY = 1; };
+template <> struct Tile2<5, 1> { static constexpr int TX = 8, TY = 1; };
+template <> struct Tile2<6, 1> { static constexpr int TX = 6, TY = 1; };
+template <> struct Tile2<7, 1> { static constexpr int TX = 4, TY = 1; };
+template <> struct Tile2<8, 1> { static constexpr int TX = 4, TY = 1; };
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled_t)p;
+    }
+    return fn;
+}
+
+// 4D map (x, y, level, field) over a rank's lattice array, box = one layer tile
+int make_tmap(CUtensorMap* m, const Geo& g, const double* base, int bx, int by, int bz) {
+    PFN_encodeTiled_t enc = encode_fn();
+    if (!enc) return fail("cuTensorMapEncodeTiled unavailable");
+    if (((uintptr_t)base & 15) || (g.px & 1)) return fail("lattice arrays must be 16-byte aligned with even pitch");
+    cuuint64_t dims[4] = {(cuuint64_t)g.lX, (cuuint64_t)g.lY, (cuuint64_t)g.Z, 5};
+    cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.lY * g.px * 8, (cuuint64_t)g.fs * 8};
+    cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz, 5};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled failed");
+    return HEVI_OK;
+}
+
+template <int N, int NY, int MODE>
+int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) {
+    constexpr int TX = Tile2<N, NY>::TX, TY = Tile2<N, NY>::TY;
+    done = false;
+    if constexpr (TX == 0) {
+        return HEVI_OK;
+    } else {
+        using T = E2<N, NY, TX, TY>;
+        const Geo& g = pl->g;
+        const size_t smem = T::fixed_bytes() + sizeof(double) * T::NTAB * g.Z;
+        if (smem > 225 * 1024) return HEVI_OK;   // v1 handles it
+        auto kern = k_explicit2<N, NY, TX, TY, MODE>;
+        static size_t attr = 0;
+        if (attr < smem) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = smem;
+        }
+        CUtensorMap tm;
+        int rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, T::NL);
+        if (rc) return rc;
+        dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
+        kern<<<grid, T::BLK, smem, st>>>(a, tm);
+        CK(cudaGetLastError());
+        done = true;
+        return HEVI_OK;
+    }
+}
+
+template <int MODE>
+int dispatch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) {
+    const int N = pl->N, Ny = pl->Ny;
+    done = false;
+    if (Ny == N) {
+        switch (N) {
+            case 1: return launch_e2<1, 1, MODE>(pl, a, st, done);
+            case 2: return launch_e2<2, 2, MODE>(pl, a, st, done);
+            case 3: return launch_e2<3, 3, MODE>(pl, a, st, done);
+            case 4: return launch_e2<4, 4, MODE>(pl, a, st, done);
+            case 5: return launch_e2<5, 5, MODE>(pl, a, st, done);
+            case 6: return launch_e2<6, 6, MODE>(pl, a, st, done);
+            case 7: return launch_e2<7, 7, MODE>(pl, a, st, done);
+        }
+    } else if (Ny == 1) {
+        switch (N) {
+            case 2: return launch_e2<2, 1, MODE>(pl, a, st, done);
+            case 3: return launch_e2<3, 1, MODE>(pl, a, st, done);
+            case 4: return launch_e2<4, 1, MODE>(pl, a, st, done);
+            case 5: return launch_e2<5, 1, MODE>(pl, a, st, done);
+            case 6: return launch_e2<6, 1, MODE>(pl, a, st, done);
+            case 7: return launch_e2<7, 1, MODE>(pl, a, st, done);
+            case 8: return launch_e2<8, 1, MODE>(pl, a, st, done);
+        }
+    }
+    return HEVI_OK;
+}
+
+int run_e2(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st, bool& done) {
+    switch (mode) {
+        case M_R: return dispatch_e2<M_R>(pl, a, st, done);
+        case M_L: return dispatch_e2<M_L>(pl, a, st, done);
+        case M_S1: return dispatch_e2<M_S1>(pl, a, st, done);
+        case M_S2: return dispatch_e2<M_S2>(pl, a, st, done);
+        case M_S3: return dispatch_e2<M_S3>(pl, a, st, done);
+    }
+    return fail("bad mode");
+}
+
 int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
+    if (pl->use_v2 && (pl->g.px % 2) == 0) {
+        bool done = false;
+        int rc = run_e2(pl, mode, a, st, done);
+        if (rc || done) return rc;
+    }
     switch (mode) {
         case M_R: return dispatch_e<M_R>(pl, a, st);
         case M_L: return dispatch_e<M_L>(pl, a, st);
@@ -960,6 +1122,8 @@ EArgs base_eargs(const hevi_plan* pl) {
     a.Dy = pl->Dy;
     a.Dz = pl->Dz;
     a.flags = pl->d_flags;
+    memcpy(a.bc, pl->bc, sizeof(a.bc));
+    a.use_tma = pl->use_tma ? 1 : 0;
     return a;
 }
 
@@ -990,7 +1154,77 @@ int launch_s(const hevi_plan* pl, SArgs a, cudaStream_t st) {
     return HEVI_OK;
 }
 
+const Factor* find_factor(const hevi_plan* pl, double lam) {
+    auto it = pl->factors.find(lam_key(lam));
+    return it == pl->factors.end() ? nullptr : &it->second;
+}
+
+template <int N>
+int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_t st) {
+    const Geo& g = pl->g;
+    const int M = g.Z;
+    S2Args a;
+    memset(&a, 0, sizeof(a));
+    a.g = g;
+    a.ph = pl->ph;
+    a.tab = f->vtab;
+    a.LU2 = f->LU2;
+    a.rU = f->rU;
+    a.Dz = pl->Dz;
+    a.ainv_identity = pl->ainv_identity;
+    a.lam = f->lam;
+    a.P = a1.P;
+    a.out = a1.out;
+    a.src_uv = a1.src_uv;
+    const int T = 128;
+    const size_t smem = sizeof(double) * ((size_t)V_NT * M + (size_t)M * (4 * N + 1) + M +
+                                          (N + 1) * (N + 1) + (size_t)M * T);
+    if (smem > 225 * 1024) return fail("column too tall for the v2 column kernel");
+    static size_t attr = 0;
+    if (attr < smem) {
+        CK(cudaFuncSetAttribute(k_solve2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+    }
+    const int NYo = g.slab ? 1 : pl->N;
+    const long long cntx = (long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0);
+    const long long cnty = (long long)(g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
+    const int blocks = (int)((cntx * cnty + T - 1) / T);
+    k_solve2<N><<<blocks, T, smem, st>>>(a);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int run_s2(const hevi_plan* pl, const Factor* f, const SArgs& a, cudaStream_t st, bool& done) {
+    done = false;
+    if (!pl->use_v2 || f->nb > 2 * pl->N + 1) return HEVI_OK;
+    const size_t need = sizeof(double) * ((size_t)V_NT * pl->g.Z +
+                                          (size_t)pl->g.Z * (4 * pl->N + 1 + 1 + 128));
+    if (need > 220 * 1024) return HEVI_OK;
+    int rc = HEVI_OK;
+    switch (pl->N) {
+        case 1: rc = launch_s2<1>(pl, f, a, st); break;
+        case 2: rc = launch_s2<2>(pl, f, a, st); break;
+        case 3: rc = launch_s2<3>(pl, f, a, st); break;
+        case 4: rc = launch_s2<4>(pl, f, a, st); break;
+        case 5: rc = launch_s2<5>(pl, f, a, st); break;
+        case 6: rc = launch_s2<6>(pl, f, a, st); break;
+        case 7: rc = launch_s2<7>(pl, f, a, st); break;
+        case 8: rc = launch_s2<8>(pl, f, a, st); break;
+        default: return HEVI_OK;
+    }
+    done = (rc == HEVI_OK);
+    return rc;
+}
+
 int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st) {
+    {
+        const Factor* f = find_factor(pl, a.lam);
+        bool done = false;
+        if (f) {
+            int rc = run_s2(pl, f, a, st, done);
+            if (rc || done) return rc;
+        }
+    }
     switch (pl->N) {
         case 1: return launch_s<1>(pl, a, st);
         case 2: return launch_s<2>(pl, a, st);
@@ -1004,10 +1238,6 @@ int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st) {
     return fail("unsupported polynomial order");
 }
 
-const Factor* find_factor(const hevi_plan* pl, double lam) {
-    auto it = pl->factors.find(lam_key(lam));
-    return it == pl->factors.end() ? nullptr : &it->second;
-}
 
 SArgs base_sargs(const hevi_plan* pl, const Factor* f) {
     SArgs a;
@@ -1088,6 +1318,10 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     h.insert(h.end(), rd->Dx, rd->Dx + nd);
     h.insert(h.end(), rd->Dy, rd->Dy + ndy);
     h.insert(h.end(), rd->Dz, rd->Dz + nd);
+    // EOS reference point per level: Pb = EOS(rho0, theta0), c0 = Pb - P0f, 1/(rho0 theta0)
+    h.insert(h.end(), rd->Pb, rd->Pb + Z);
+    for (int k = 0; k < Z; ++k) h.push_back(rd->Pb[k] - rd->P0f[k]);
+    for (int k = 0; k < Z; ++k) h.push_back(1.0 / (rd->rho0[k] * rd->theta0[k]));
     pl->ainv_identity = 1;
     for (int k = 0; k < Z; ++k)
         if (rd->dtheta0[k] != 0.0) pl->ainv_identity = 0;
@@ -1101,13 +1335,26 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
         return fail("plan allocation", e);
     }
     const double* d = pl->d_tab;
-    pl->lv = {d, d + Z, d + 2 * Z, d + 3 * Z, d + 4 * Z, d + 5 * Z, d + 6 * Z, d + 7 * Z, d + 8 * Z};
     pl->cx = d + 9 * Z;
     pl->cy = pl->cx + X;
     pl->cz = pl->cy + Y;
     pl->Dx = pl->cz + Z;
     pl->Dy = pl->Dx + nd;
     pl->Dz = pl->Dy + ndy;
+    const double* eos = pl->Dz + nd;
+    pl->lv = {d,         d + Z,     d + 2 * Z, d + 3 * Z, d + 4 * Z, d + 5 * Z,
+              d + 6 * Z, d + 7 * Z, d + 8 * Z, eos,       eos + Z,   eos + 2 * Z};
+    // binomial coefficients C(gamma, k) of the P' series
+    {
+        double cb = 1.0;
+        for (int k = 1; k <= 15; ++k) {
+            cb = cb * (rd->gamma - (k - 1)) / k;
+            pl->bc[k - 1] = cb;
+        }
+        pl->bc[15] = 0.0;
+    }
+    pl->use_v2 = getenv("HEVI_KERNELS") == nullptr || strcmp(getenv("HEVI_KERNELS"), "v1") != 0;
+    pl->use_tma = getenv("HEVI_NO_TMA") == nullptr;
     *out = pl;
     return HEVI_OK;
 }
@@ -1119,6 +1366,9 @@ int hevi_plan_destroy(hevi_plan* pl) {
         cudaFree(kv.second.LU);
         cudaFree(kv.second.LUb);
         cudaFree(kv.second.lamtab);
+        cudaFree(kv.second.vtab);
+        cudaFree(kv.second.LU2);
+        cudaFree(kv.second.rU);
         cudaFree(kv.second.d_nb);
     }
     cudaFree(pl->d_tab);
@@ -1144,6 +1394,9 @@ int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
         CK(cudaMalloc(&f.LU, sizeof(double) * M * M));
         CK(cudaMalloc(&f.LUb, sizeof(double) * M * (2 * M - 1)));
         CK(cudaMalloc(&f.lamtab, sizeof(double) * 3 * M));
+        CK(cudaMalloc(&f.vtab, sizeof(double) * 12 * M));
+        CK(cudaMalloc(&f.LU2, sizeof(double) * M * (4 * pl->N + 1)));
+        CK(cudaMalloc(&f.rU, sizeof(double) * M));
         CK(cudaMalloc(&f.d_nb, sizeof(int)));
         CK(cudaMemsetAsync(f.A, 0, sizeof(double) * M * M, st));
         FArgs a;
@@ -1157,13 +1410,15 @@ int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
         a.M = M;
         a.ainv_identity = pl->ainv_identity;
         a.lamtab = f.lamtab;
+        a.vtab = f.vtab;
         a.A = f.A;
         a.flags = pl->d_flags;
         k_lamtab<<<(M + 127) / 128, 128, 0, st>>>(a);
         CK(cudaGetLastError());
         k_probe<<<(M + 63) / 64, 64, 0, st>>>(a);
         CK(cudaGetLastError());
-        k_lu_dense<<<1, 256, 0, st>>>(f.A, f.LU, f.LUb, M, f.d_nb, pl->d_flags);
+        k_lu_dense<<<1, 256, 0, st>>>(f.A, f.LU, f.LUb, M, f.d_nb, pl->d_flags, pl->N, f.LU2,
+                                      f.rU);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(&f.nb, f.d_nb, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));

@@ -1,0 +1,226 @@
+// solve_v2.cuh -- production column kernel (included by hevi.cu inside its
+// anonymous namespace).
+//
+// One thread per vertical column, fused:
+//   forward  (bottom -> top, one element of N levels per iteration):
+//     Schur RHS  Pe - lam (F0 ua + rho0 G0 d/dz ua)   (imexcore.py:229-243)
+//     and forward substitution with L                 (columnsolve.py:172-174)
+//   backward (top -> bottom):
+//     back substitution with U                        (columnsolve.py:176-180)
+//     and, one element behind, the extraction of w, theta', rho'
+//                                                     (imexcore.py:273-287)
+// The element's ua / y / x values live in register windows (static indices
+// after unrolling), the forward results y in shared memory; the band LU
+// (shared by all columns on box meshes) is read from shared memory with a
+// fixed width of 2N sub/super-diagonals (the Schur column bandwidth is 2N+1).
+#pragma once
+
+struct S2Args {
+    Geo g;
+    Phys ph;
+    const double* tab;   // 12 x M level tables (see k_lu_dense2 / plan)
+    const double* LU2;   // M x (4N+1), d = j - k + 2N
+    const double* rU;    // 1/U_kk
+    const double* Dz;
+    int ainv_identity;
+    double lam;
+    const double* P;       // predictor fields 0,3,4
+    double* out;           // writes fields 0,3,4
+    const double* src_uv;  // optional: copy u,v (with no-flux zeroing)
+};
+
+enum { V_G0 = 0, V_H0, V_F0Z, V_RG, V_CZ, V_COEF, V_UA, V_DEN, V_DTH0, V_IRHO0, V_IG0R, V_IG0, V_NT };
+
+template <int N>
+__global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
+    constexpr int W = 4 * N + 1;
+    extern __shared__ __align__(16) double sm2[];
+    const Geo& g = a.g;
+    const int M = g.Z;
+    const int T = blockDim.x;
+    const int tid = threadIdx.x;
+    double* tb = sm2;                  // V_NT * M
+    double* LU = tb + V_NT * M;        // M * W
+    double* rU = LU + M * W;           // M
+    double* sD = rU + M;               // (N+1)^2
+    double* Y = sD + (N + 1) * (N + 1);  // M * T
+    for (int i = tid; i < V_NT * M; i += T) tb[i] = a.tab[i];
+    for (int i = tid; i < M * W; i += T) LU[i] = a.LU2[i];
+    for (int i = tid; i < M; i += T) rU[i] = a.rU[i];
+    for (int i = tid; i < (N + 1) * (N + 1); i += T) sD[i] = a.Dz[i];
+    __syncthreads();
+
+    const int NYo = g.slab ? 1 : N;
+    const int xlo = g.ex_b * N;
+    const int cntx = (g.ex_e - g.ex_b) * N + (g.ex_e == g.nex ? 1 : 0);
+    const int ylo = g.ey_b * NYo;
+    const int cnty = (g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
+    const int c = blockIdx.x * T + tid;
+    if (c >= cntx * cnty) return;
+    const int gx = xlo + c % cntx;
+    const int gy = ylo + c / cntx;
+    const int gys = g.slab ? 0 : gy;
+    const long long fs = g.fs;
+    const double lam = a.lam, gr = a.ph.g;
+    const bool ident = a.ainv_identity != 0;
+    const int nez = g.nez;
+    const double* Ps = a.P + loff(g, gx, gys, 0);   // source column (slab: y = 0)
+    const double* Po = a.P + loff(g, gx, gy, 0);    // own column
+    double* Oo = a.out + loff(g, gx, gy, 0);
+    const long long ls = (long long)g.lY * g.px;    // level stride
+#define TB(t, k) tb[(t) * M + (k)]
+
+    auto ua_of = [&](double we, double te, int k) -> double {
+        double v = we + (TB(V_COEF, k) * te) * gr;
+        if (!ident) v = v - TB(V_UA, k) * ((TB(V_DTH0, k) * v) / TB(V_DEN, k));
+        return (k == 0 || k == M - 1) ? 0.0 : v;
+    };
+
+    // ---------------- forward: RHS + L substitution --------------------------
+    double uaw[N + 1], Pew[N + 1], yw[3 * N];
+#pragma unroll
+    for (int i = 0; i < 3 * N; ++i) yw[i] = 0.0;
+    {
+        const double re = Ps[0], we = Ps[3 * fs], te = Ps[4 * fs];
+        uaw[0] = ua_of(we, te, 0);
+        Pew[0] = TB(V_G0, 0) * re + TB(V_H0, 0) * te;
+    }
+    double carry = 0.0;
+    for (int e = 0; e < nez; ++e) {
+        const int k0 = e * N;
+        double re[N], we[N], te[N];
+#pragma unroll
+        for (int l = 1; l <= N; ++l) {
+            const long long o = (long long)(k0 + l) * ls;
+            re[l - 1] = Ps[o];
+            we[l - 1] = Ps[o + 3 * fs];
+            te[l - 1] = Ps[o + 4 * fs];
+        }
+#pragma unroll
+        for (int l = 1; l <= N; ++l) {
+            const int k = k0 + l;
+            uaw[l] = ua_of(we[l - 1], te[l - 1], k);
+            Pew[l] = TB(V_G0, k) * re[l - 1] + TB(V_H0, k) * te[l - 1];
+        }
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+            const int k = k0 + l;
+            double d = 0.0;
+#pragma unroll
+            for (int m = 0; m <= N; ++m) d = fma(sD[l * (N + 1) + m], uaw[m], d);
+            if (l == 0 && e > 0) d += carry;
+            const double dua = TB(V_CZ, k) * d;
+            const double rhs = Pew[l] - lam * (TB(V_F0Z, k) * uaw[l] + TB(V_RG, k) * dua);
+            double s = 0.0;
+            const double* Lr = LU + k * W;
+#pragma unroll
+            for (int j = 1; j <= 2 * N; ++j) s = fma(Lr[2 * N - j], yw[2 * N + l - j], s);
+            const double y = rhs - s;
+            yw[2 * N + l] = y;
+            Y[k * T + tid] = y;
+        }
+        // row N of this element: the lower half of the next face derivative
+        double cr = 0.0;
+#pragma unroll
+        for (int m = 0; m <= N; ++m) cr = fma(sD[N * (N + 1) + m], uaw[m], cr);
+        carry = cr;
+        if (e + 1 < nez) {
+#pragma unroll
+            for (int i = 0; i < 2 * N; ++i) yw[i] = yw[i + N];
+            uaw[0] = uaw[N];
+            Pew[0] = Pew[N];
+        }
+    }
+    {   // top level: row N of the last element, boundary
+        const int k = M - 1;
+        const double dua = TB(V_CZ, k) * carry;
+        const double rhs = Pew[N] - lam * (TB(V_F0Z, k) * uaw[N] + TB(V_RG, k) * dua);
+        double s = 0.0;
+        const double* Lr = LU + k * W;
+#pragma unroll
+        for (int j = 1; j <= 2 * N; ++j) s = fma(Lr[2 * N - j], yw[3 * N - j], s);
+        Y[k * T + tid] = rhs - s;
+    }
+
+    // ---------------- backward: U substitution + extraction -------------------
+    // xw[l] = x_{k0 + l}, l = 0 .. 3N (current element and 2N levels above)
+    double xw[3 * N + 1];
+#pragma unroll
+    for (int i = 0; i <= 3 * N; ++i) xw[i] = 0.0;
+    xw[N] = Y[(M - 1) * T + tid] * rU[M - 1];
+
+    auto extract = [&](int k, double Pk, double dsum, double we, double te) {
+        const bool bz = (k == 0) || (k == M - 1);
+        const double dP = TB(V_CZ, k) * dsum;
+        double up = lam * (dP * TB(V_IRHO0, k) + (Pk * TB(V_IG0R, k)) * gr);
+        double ua = we + (TB(V_COEF, k) * te) * gr;
+        if (!ident) {
+            ua = ua - TB(V_UA, k) * ((TB(V_DTH0, k) * ua) / TB(V_DEN, k));
+            up = up - TB(V_UA, k) * ((TB(V_DTH0, k) * up) / TB(V_DEN, k));
+        }
+        if (bz) {
+            ua = 0.0;
+            up = 0.0;
+        }
+        const double w = ua - up;
+        const double th = te - lam * (w * TB(V_DTH0, k));
+        const double rho = (Pk - TB(V_H0, k) * th) * TB(V_IG0, k);
+        const long long o = (long long)k * ls;
+        Oo[o] = rho;
+        Oo[o + 3 * fs] = w;
+        Oo[o + 4 * fs] = th;
+        if (a.src_uv) {
+            const bool bx = (gx == 0) || (gx == g.X - 1);
+            const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
+            const double* su = a.src_uv + loff(g, gx, gy, k);
+            Oo[o + fs] = bx ? 0.0 : su[fs];
+            Oo[o + 2 * fs] = by ? 0.0 : su[2 * fs];
+        }
+    };
+
+    for (int e = nez - 1; e >= 0; --e) {
+        const int k0 = e * N;
+        double we[N], te[N];
+#pragma unroll
+        for (int l = 1; l <= N; ++l) {
+            const long long o = (long long)(k0 + l) * ls;
+            we[l - 1] = Po[o + 3 * fs];
+            te[l - 1] = Po[o + 4 * fs];
+        }
+#pragma unroll
+        for (int l = N - 1; l >= 0; --l) {
+            const int k = k0 + l;
+            double s = 0.0;
+            const double* Ur = LU + k * W + 2 * N;
+#pragma unroll
+            for (int j = 1; j <= 2 * N; ++j) s = fma(Ur[j], xw[l + j], s);
+            xw[l] = (Y[k * T + tid] - s) * rU[k];
+        }
+        // extraction of levels k0+1 .. k0+N (element e now complete)
+#pragma unroll
+        for (int l = 1; l <= N; ++l) {
+            const int k = k0 + l;
+            double d = 0.0;
+#pragma unroll
+            for (int m = 0; m <= N; ++m) d = fma(sD[l * (N + 1) + m], xw[m], d);
+            if (l == N && e + 1 < nez) {
+                double d2 = 0.0;
+#pragma unroll
+                for (int m = 0; m <= N; ++m) d2 = fma(sD[m], xw[N + m], d2);
+                d += d2;
+            }
+            extract(k, xw[l], d, we[l - 1], te[l - 1]);
+        }
+        if (e > 0) {
+#pragma unroll
+            for (int i = 2 * N; i >= 0; --i) xw[N + i] = xw[i];
+        }
+    }
+    {   // bottom level: row 0 of element 0, boundary
+        double d = 0.0;
+#pragma unroll
+        for (int m = 0; m <= N; ++m) d = fma(sD[m], xw[m], d);
+        extract(0, xw[0], d, Po[3 * fs], Po[4 * fs]);
+    }
+#undef TB
+}

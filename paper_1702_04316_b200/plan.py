@@ -45,16 +45,20 @@ class HeviPlan:
         if window is None:
             window = dict(x0=0, y0=0, lX=X, lY=Y, ex_b=0, ex_e=mesh.nx, ey_b=0, ey_e=mesh.ny)
         self.window = window
-        px = window.get("px", window["lX"])
+        # even pitch (TMA strides are 16-byte multiples), rows 32-byte aligned
+        px = window.get("px", (window["lX"] + 3) // 4 * 4)
         gd = nv.GridDesc(nex=mesh.nx, ney=mesh.ny, nez=mesh.nz, N=mesh.N, Ny=mesh.Ny,
                          slab=int(mesh.slab), x0=window["x0"], y0=window["y0"],
                          lX=window["lX"], lY=window["lY"], px=px,
                          ex_b=window["ex_b"], ex_e=window["ex_e"],
                          ey_b=window["ey_b"], ey_e=window["ey_e"])
         c = ref.const
+        # EOS of the background per level, evaluated exactly as
+        # euler.equation_of_state (euler.py:185): the reference point of P'
+        Pb = c.P0 * (ref.rho0 * c.R * ref.theta0 / c.P0) ** c.gamma
         self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (
             ref.rho0, ref.theta0, ref.P0f, ref.drho0, ref.dtheta0, ref.G0_nc, ref.H0_nc,
-            ref.F0z_nc, ref.rho0G0, disc.cx, disc.cy, disc.cz,
+            ref.F0z_nc, ref.rho0G0, Pb, disc.cx, disc.cy, disc.cz,
             mesh.quad_r.D, mesh.quad_s.D, mesh.quad_t.D)]
         rd = nv.RefDesc(*[_dp(a) for a in self._keep], c.g, c.R, c.P0, c.gamma)
         h = ctypes.c_void_p()
@@ -89,6 +93,14 @@ class HeviPlan:
         return torch.zeros((4,) + self.shape, dtype=torch.float64, device=self.device)
 
     # -- conversions -----------------------------------------------------------
+    def padded(self, L):
+        """(nf, Z, lY, lX) -> plan layout (nf, Z, lY, px)."""
+        if L.shape[-1] == self.px:
+            return L.contiguous()
+        out = self.zeros(L.shape[0])
+        out[..., :L.shape[-1]].copy_(L)
+        return out
+
     def e2l(self, E, out=None, nf=None):
         nf = E.shape[0] if nf is None else nf
         out = self.zeros(nf) if out is None else out
@@ -97,6 +109,7 @@ class HeviPlan:
 
     def l2e(self, L, out=None):
         import torch
+        L = self.padded(L)
         nf = L.shape[0]
         if out is None:
             out = torch.empty((nf,) + tuple(self.mesh.nshape), dtype=torch.float64, device=self.device)
@@ -177,7 +190,13 @@ def to_device(q):
         t = q.to(device="cuda", dtype=torch.float64).contiguous()
         if dev.type == "cuda":
             return t, (lambda r: r)
-        return t, (lambda r: r.to(dev))
+
+        def back(r):
+            # host results land in (cached) pinned memory: full-bandwidth D2H
+            out = torch.empty(r.shape, dtype=r.dtype, pin_memory=True)
+            out.copy_(r)
+            return out
+        return t, back
     arr = np.ascontiguousarray(q, dtype=np.float64)
     t = torch.from_numpy(arr).to("cuda")
     return t, (lambda r: r.cpu().numpy())
