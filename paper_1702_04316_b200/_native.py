@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhevi.so")
+LIB_PATH = os.environ.get("HEVI_LIB") or os.path.join(_HERE, "_lib", "libhevi.so")
 
 HEVI_OK = 0
 F_NONFINITE_OUT = 1 << 12

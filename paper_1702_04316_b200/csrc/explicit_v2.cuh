@@ -22,6 +22,9 @@
 //      L_V(q) pointwise, no-flux projection, fused ARK2 stage epilogue.
 #pragma once
 
+template <int N, int NY>
+struct Tile2;   // TX, TY, MINB (defined with the dispatch in hevi.cu)
+
 template <int N, int NY, int TX, int TY>
 struct E2 {
     static constexpr int OX = TX * N;                         // main x points per tile
@@ -34,7 +37,8 @@ struct E2 {
     static constexpr int LY = TY * NY + NY + 1;
     static constexpr int NL = N + 1;                          // level slots (ring)
     static constexpr int PL = LY * LXT;                       // one level plane
-    static constexpr int NT = OX * OYM * N;                   // main points == threads
+    static constexpr int K = (N % 2 == 0) ? 2 : 1;             // vertical points per thread
+    static constexpr int NT = OX * OYM * (N / K);             // main threads
     static constexpr int BLK = (NT + 31) / 32 * 32;
     static constexpr int CXW = OX + 1, CYW = TY * NY + 1 + (NY == 1 ? 1 : 0);
     static constexpr int STG_N = 5 * NL * PL;                 // TMA staging
@@ -102,9 +106,9 @@ __device__ __forceinline__ double pprime(double r, double th, double rho0, doubl
     return ph.P0 * pow(rho * ph.R * theta / ph.P0, ph.gamma) - P0f;
 }
 
-template <int N, int NY>
+template <int N, int NY, int K>
 struct DRows {
-    double x[N + 1], y[NY + 1], z[N + 1];   // the point's own rows; face rows (row N) from smem
+    double x[N + 1], y[NY + 1], z[K][N + 1];   // the points' own rows; face rows (row N) from smem
 };
 
 // per-axis geometry of one point inside the tile
@@ -128,205 +132,246 @@ __device__ __forceinline__ PAx pax(int gi, int l, int N, int ne) {
     return r;
 }
 
-template <int N, int NY, int TX, int TY, int MODE, bool MAIN>
-__device__ __forceinline__ void e2_point(const EArgs& a, const double* __restrict__ S,
-                                         const double* __restrict__ CARp,
-                                         const double* __restrict__ XF, const double* __restrict__ LT,
-                                         const DRows<N, NY>& D, const double* __restrict__ sDx,
-                                         const double* __restrict__ sDy, const PAx& ax, const PAx& ay,
-                                         int oz, int ox, int oy, int gx, int gy, int gz, int ez,
-                                         double cx, double cy, int Z) {
+// K vertically adjacent points (levels oz0 .. oz0+K-1 of one column) per
+// thread: x/y rows and set-up are shared, every z-line is loaded once for
+// all K points, and the K derivative chains are independent (ILP).
+template <int N, int NY, int TX, int TY, int MODE, bool MAIN, int K>
+__device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict__ S,
+                                       const double* __restrict__ CARp, double* __restrict__ CARw,
+                                       const double* __restrict__ XF, const double* __restrict__ LT,
+                                       const DRows<N, NY, K>& D, const double* __restrict__ sDx,
+                                       const double* __restrict__ sDy, const PAx& ax, const PAx& ay,
+                                       int oz0, int ox, int oy, int gx, int gy, int ez, double cx,
+                                       double cy, int Z) {
     using T = E2<N, NY, TX, TY>;
     constexpr int PL = T::PL, LXT = T::LXT, NL = T::NL;
     constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
     constexpr bool NEED_R = (MODE != M_L);
     const Geo& g = a.g;
-    const long long o = loff(g, gx, gy, gz);
     const long long fs = g.fs;
-    // stage inputs read pointwise: issue early, consume in the epilogue
-    double Ain[5], Fin[5];
-    if (MODE == M_S2) {
-#pragma unroll
-        for (int f = 0; f < 5; ++f) Ain[f] = a.A[o + f * fs];
-    }
-    if (MODE == M_S2 || MODE == M_S3) {
-#pragma unroll
-        for (int f = 0; f < 5; ++f) Fin[f] = a.F[o + f * fs];
-    }
     const int base = ez * N;
-    const int sl = (base + oz) % NL;
+    long long o[K];
+    int sl[K], gzk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        gzk[k] = base + oz0 + k;
+        o[k] = loff(g, gx, gy, gzk[k]);
+        sl[k] = (base + oz0 + k) % NL;
+    }
+    // stage inputs read pointwise: issue early, consume in the epilogue
+    double Ain[K][5], Fin[K][5];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (MODE == M_S2) {
+#pragma unroll
+            for (int f = 0; f < 5; ++f) Ain[k][f] = a.A[o[k] + f * fs];
+        }
+        if (MODE == M_S2 || MODE == M_S3) {
+#pragma unroll
+            for (int f = 0; f < 5; ++f) Fin[k][f] = a.F[o[k] + f * fs];
+        }
+    }
     int zs[N + 1];
 #pragma unroll
     for (int m = 0; m <= N; ++m) zs[m] = ((base + m) % NL) * PL;
-    const double cz = LT[T_CZ * Z + gz];
     const int cidx = oy * T::CXW + ox;
-    const int pnt = sl * PL + ay.l * LXT + ax.l;
+    const bool do_carry = (oz0 == 0) && (ez + 1 < g.nez);
+    const bool zface = (oz0 == 0) && (ez > 0);
+    const double* Sxy = S + ay.l * LXT + ax.l;   // column base (plus f*NL*PL + slot*PL)
 
-    // pointwise values first: every derivative is folded into the
-    // accumulators as soon as it is formed (R is affine in the gradients)
-    const double r = S[0 * NL * PL + pnt], u = S[1 * NL * PL + pnt], v = S[2 * NL * PL + pnt],
-                 w = S[3 * NL * PL + pnt], th = S[4 * NL * PL + pnt];
-    const double rho0 = LT[T_RHO0 * Z + gz];
-    const double rho = rho0 + r;
-    const double rinv = 1.0 / rho;
-    const double gr = a.ph.g;
-    // one field's (d/dx, d/dy, d/dz) at the point, DSS-averaged (folded)
-    auto grad = [&](int f, double& gx_, double& gy_, double& gz_, bool want_xy) {
+    double r[K], u[K], v[K], w[K], th[K], rho[K], rinv[K], cz[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double* pp = Sxy + sl[k] * PL;
+        r[k] = pp[0 * NL * PL];
+        u[k] = pp[1 * NL * PL];
+        v[k] = pp[2 * NL * PL];
+        w[k] = pp[3 * NL * PL];
+        th[k] = pp[4 * NL * PL];
+        rho[k] = LT[T_RHO0 * Z + gzk[k]] + r[k];
+        rinv[k] = 1.0 / rho[k];
+        cz[k] = LT[T_CZ * Z + gzk[k]];
+    }
+    // d/dx, d/dy, d/dz of field f at the K points (DSS-averaged, folded)
+    auto grad = [&](int f, bool want_xy, double (&gxv)[K], double (&gyv)[K], double (&gzv)[K]) {
         const double* Sf = S + f * (NL * PL);
         if (want_xy) {
-            const double* sx = Sf + sl * PL + ay.l * LXT + ax.s0;
-            double d = 0.0;
 #pragma unroll
-            for (int m = 0; m <= N; ++m) d = fma(D.x[m], sx[m], d);
-            if (ax.face) {
-                if (MAIN) {
-                    d += XF[((f * TX + ox / N) * T::OYM + oy) * N + oz];
-                } else {
-                    const double* sxl = Sf + sl * PL + ay.l * LXT + ax.l - N;
-                    double e = 0.0;
+            for (int k = 0; k < K; ++k) {
+                const double* sx = Sf + sl[k] * PL + ay.l * LXT + ax.s0;
+                double d = 0.0;
 #pragma unroll
-                    for (int m = 0; m <= N; ++m) e = fma(sDx[N * (N + 1) + m], sxl[m], e);
-                    d += e;
+                for (int m = 0; m <= N; ++m) d = fma(D.x[m], sx[m], d);
+                if (ax.face) {
+                    if (MAIN) {
+                        d += XF[((f * TX + ox / N) * T::OYM + oy) * N + oz0 + k];
+                    } else {
+                        const double* sxl = Sf + sl[k] * PL + ay.l * LXT + ax.l - N;
+                        double e = 0.0;
+#pragma unroll
+                        for (int m = 0; m <= N; ++m) e = fma(sDx[N * (N + 1) + m], sxl[m], e);
+                        d += e;
+                    }
                 }
-            }
-            gx_ = cx * d;
-            const double* sy = Sf + sl * PL + ay.s0 * LXT + ax.l;
-            double e = 0.0;
+                gxv[k] = cx * d;
+                const double* sy = Sf + sl[k] * PL + ay.s0 * LXT + ax.l;
+                double e = 0.0;
 #pragma unroll
-            for (int m = 0; m <= NY; ++m) e = fma(D.y[m], sy[m * LXT], e);
-            if (ay.face) {
-                const double* syl = Sf + sl * PL + (ay.l - NY) * LXT + ax.l;
-                double h = 0.0;
+                for (int m = 0; m <= NY; ++m) e = fma(D.y[m], sy[m * LXT], e);
+                if (ay.face) {
+                    const double* syl = Sf + sl[k] * PL + (ay.l - NY) * LXT + ax.l;
+                    double h = 0.0;
 #pragma unroll
-                for (int m = 0; m <= NY; ++m) h = fma(sDy[NY * (NY + 1) + m], syl[m * LXT], h);
-                e += h;
+                    for (int m = 0; m <= NY; ++m) h = fma(sDy[NY * (NY + 1) + m], syl[m * LXT], h);
+                    e += h;
+                }
+                gyv[k] = cy * e;
             }
-            gy_ = cy * e;
         }
         const double* sz = Sf + ay.l * LXT + ax.l;
-        double d = 0.0;
+        double val[N + 1];
 #pragma unroll
-        for (int m = 0; m <= N; ++m) d = fma(D.z[m], sz[zs[m]], d);
-        if (oz == 0 && ez > 0) d += CARp[f * (T::CYW * T::CXW) + cidx];
-        gz_ = cz * d;
-    };
-    double R0 = 0.0, R1 = 0.0, R2 = 0.0, R3 = 0.0, R4 = 0.0;
-    double dwz = 0.0, dPLz = 0.0;
-    {
-        double gxv, gyv, gzv;
-        double divu;
-        if (NEED_R) {
-            grad(0, gxv, gyv, gzv, true);
-            R0 = (u * gxv + v * gyv) + w * gzv;                       // u . grad rho'
-            grad(1, gxv, gyv, gzv, true);
-            R1 = (u * gxv + v * gyv) + w * gzv;
-            divu = gxv;
-            grad(2, gxv, gyv, gzv, true);
-            R2 = (u * gxv + v * gyv) + w * gzv;
-            divu += gyv;
+        for (int m = 0; m <= N; ++m) val[m] = sz[zs[m]];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double d = 0.0;
+#pragma unroll
+            for (int m = 0; m <= N; ++m) d = fma(D.z[k][m], val[m], d);
+            if (k == 0 && zface) d += CARp[f * (T::CYW * T::CXW) + cidx];
+            gzv[k] = cz[k] * d;
         }
-        grad(3, gxv, gyv, gzv, NEED_R);
-        dwz = gzv;
+        if (do_carry) {
+            double top = 0.0;
+#pragma unroll
+            for (int m = 0; m <= N; ++m) top = fma(sDx[N * (N + 1) + m], val[m], top);
+            CARw[f * (T::CYW * T::CXW) + cidx] = top;
+        }
+    };
+    double R0[K], R1[K], R2[K], R3[K], R4[K], dwz[K], dPLz[K];
+    {
+        double gxv[K], gyv[K], gzv[K], divu[K];
         if (NEED_R) {
-            R3 = (u * gxv + v * gyv) + w * gzv;
-            divu += gzv;
-            grad(4, gxv, gyv, gzv, true);
-            R4 = (u * gxv + v * gyv) + w * gzv;
-            grad(5, gxv, gyv, gzv, true);                              // grad P'
-            R1 += gxv * rinv;
-            R2 += gyv * rinv;
-            R3 += gzv * rinv;
-            R0 += rho * divu;
+            grad(0, true, gxv, gyv, gzv);
+#pragma unroll
+            for (int k = 0; k < K; ++k) R0[k] = (u[k] * gxv[k] + v[k] * gyv[k]) + w[k] * gzv[k];
+            grad(1, true, gxv, gyv, gzv);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                R1[k] = (u[k] * gxv[k] + v[k] * gyv[k]) + w[k] * gzv[k];
+                divu[k] = gxv[k];
+            }
+            grad(2, true, gxv, gyv, gzv);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                R2[k] = (u[k] * gxv[k] + v[k] * gyv[k]) + w[k] * gzv[k];
+                divu[k] += gyv[k];
+            }
+        }
+        grad(3, NEED_R, gxv, gyv, gzv);
+#pragma unroll
+        for (int k = 0; k < K; ++k) dwz[k] = gzv[k];
+        if (NEED_R) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                R3[k] = (u[k] * gxv[k] + v[k] * gyv[k]) + w[k] * gzv[k];
+                divu[k] += gzv[k];
+            }
+            grad(4, true, gxv, gyv, gzv);
+#pragma unroll
+            for (int k = 0; k < K; ++k) R4[k] = (u[k] * gxv[k] + v[k] * gyv[k]) + w[k] * gzv[k];
+            grad(5, true, gxv, gyv, gzv);   // grad P'
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                R1[k] += gxv[k] * rinv[k];
+                R2[k] += gyv[k] * rinv[k];
+                R3[k] += gzv[k] * rinv[k];
+                R0[k] += rho[k] * divu[k];
+            }
         }
         if (NEED_L) {
-            double dummy_x = 0.0, dummy_y = 0.0;
-            grad(6, dummy_x, dummy_y, gzv, false);                      // d/dz of linearised P
-            dPLz = gzv;
+            grad(6, false, gxv, gyv, gzv);   // d/dz of the linearised pressure
+#pragma unroll
+            for (int k = 0; k < K; ++k) dPLz[k] = gzv[k];
         }
     }
-    const double drho0 = LT[T_DRHO0 * Z + gz];
-    const double dth0 = LT[T_DTH0 * Z + gz];
+    const double gr = a.ph.g;
     const bool bx = (gx == 0) || (gx == g.X - 1);
     const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
-    const bool bz = (gz == 0) || (gz == g.Z - 1);
-    if (NEED_R) {
-        const double theta = LT[T_TH0 * Z + gz] + th;
-        if (!(isfinite(r) && isfinite(u) && isfinite(v) && isfinite(w) && isfinite(th)))
-            atomicOr(a.flags, HEVI_F_NONFINITE_IN(a.stage));
-        if (!(rho > 0.0) || !(theta > 0.0)) atomicOr(a.flags, HEVI_F_EOS(a.stage));
-        // euler.nonlinear_rhs set2nc (euler.py:458-473), DSS folded into the derivatives
-        R0 = -(R0 + w * drho0);
-        R1 = -R1;
-        R2 = -R2;
-        R3 = -(R3 + (r * rinv) * gr);
-        R4 = -(R4 + w * dth0);
-        if (bx) R1 = 0.0;
-        if (by) R2 = 0.0;
-        if (bz) R3 = 0.0;
-    }
-    double L0 = 0.0, L3 = 0.0, L4 = 0.0;
-    if (NEED_L) {
-        // euler.linear_operator(vertical_only=True), set2nc (euler.py:333-361)
-        const double irho0 = LT[T_IRHO0 * Z + gz];
-        L0 = -(w * drho0 + rho0 * dwz);
-        L3 = bz ? 0.0 : -(dPLz * irho0 + (r * irho0) * gr);
-        L4 = -(w * dth0);
-    }
-    if (MODE == M_R) {
-        a.out[o] = R0;
-        a.out[o + fs] = R1;
-        a.out[o + 2 * fs] = R2;
-        a.out[o + 3 * fs] = R3;
-        a.out[o + 4 * fs] = R4;
-    } else if (MODE == M_L) {
-        a.out[o] = L0;
-        a.out[o + fs] = 0.0;
-        a.out[o + 2 * fs] = 0.0;
-        a.out[o + 3 * fs] = L3;
-        a.out[o + 4 * fs] = L4;
-    } else if (MODE == M_S1) {
-        // imexcore.ark_imex_step (imexcore.py:398-403, 409-411)
-        const double dt = a.dt;
-        const double qv[5] = {r, u, v, w, th};
-        const double Rv[5] = {R0, R1, R2, R3, R4};
-        const double Lv[5] = {L0, 0.0, 0.0, L3, L4};
-        double pr[5];
 #pragma unroll
-        for (int f = 0; f < 5; ++f) {
-            pr[f] = qv[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
-            a.A[o + f * fs] = qv[f] + dt * (a.a_a * (Rv[f] - Lv[f]) + a.at_a * Lv[f]);
-            a.F[o + f * fs] = qv[f] + a.cb * Rv[f];
+    for (int k = 0; k < K; ++k) {
+        const int gz = gzk[k];
+        const double drho0 = LT[T_DRHO0 * Z + gz];
+        const double dth0 = LT[T_DTH0 * Z + gz];
+        const bool bz = (gz == 0) || (gz == g.Z - 1);
+        double Rv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        if (NEED_R) {
+            const double theta = LT[T_TH0 * Z + gz] + th[k];
+            if (!(isfinite(r[k]) && isfinite(u[k]) && isfinite(v[k]) && isfinite(w[k]) &&
+                  isfinite(th[k])))
+                atomicOr(a.flags, HEVI_F_NONFINITE_IN(a.stage));
+            if (!(rho[k] > 0.0) || !(theta > 0.0)) atomicOr(a.flags, HEVI_F_EOS(a.stage));
+            // euler.nonlinear_rhs set2nc (euler.py:458-473), DSS folded into the derivatives;
+            // euler.zero_normal_velocity after the DSS (euler.py:494-496)
+            Rv[0] = -(R0[k] + w[k] * drho0);
+            Rv[1] = bx ? 0.0 : -R1[k];
+            Rv[2] = by ? 0.0 : -R2[k];
+            Rv[3] = bz ? 0.0 : -(R3[k] + (r[k] * rinv[k]) * gr);
+            Rv[4] = -(R4[k] + w[k] * dth0);
         }
-        a.P[o] = pr[0];
-        a.P[o + 3 * fs] = pr[3];
-        a.P[o + 4 * fs] = pr[4];
-        a.Quv[o + fs] = bx ? 0.0 : pr[1];
-        a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
-    } else if (MODE == M_S2) {
-        const double dt = a.dt;
-        const double Rv[5] = {R0, R1, R2, R3, R4};
-        const double Lv[5] = {L0, 0.0, 0.0, L3, L4};
-        double pr[5];
+        double Lv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        if (NEED_L) {
+            // euler.linear_operator(vertical_only=True), set2nc (euler.py:333-361)
+            const double irho0 = LT[T_IRHO0 * Z + gz];
+            Lv[0] = -(w[k] * drho0 + LT[T_RHO0 * Z + gz] * dwz[k]);
+            Lv[3] = bz ? 0.0 : -(dPLz[k] * irho0 + (r[k] * irho0) * gr);
+            Lv[4] = -(w[k] * dth0);
+        }
+        const long long oo = o[k];
+        if (MODE == M_R) {
 #pragma unroll
-        for (int f = 0; f < 5; ++f) {
-            pr[f] = Ain[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
-            a.F[o + f * fs] = Fin[f] + a.cb * Rv[f];
-        }
-        a.P[o] = pr[0];
-        a.P[o + 3 * fs] = pr[3];
-        a.P[o + 4 * fs] = pr[4];
-        a.Quv[o + fs] = bx ? 0.0 : pr[1];
-        a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
-    } else {
-        const double Rv[5] = {R0, R1, R2, R3, R4};
-        bool fin = true;
+            for (int f = 0; f < 5; ++f) a.out[oo + f * fs] = Rv[f];
+        } else if (MODE == M_L) {
 #pragma unroll
-        for (int f = 0; f < 5; ++f) {
-            const double val = Fin[f] + a.cb * Rv[f];
-            fin = fin && isfinite(val);
-            a.out[o + f * fs] = val;
+            for (int f = 0; f < 5; ++f) a.out[oo + f * fs] = Lv[f];
+        } else if (MODE == M_S1) {
+            // imexcore.ark_imex_step (imexcore.py:398-403, 409-411)
+            const double dt = a.dt;
+            const double qv[5] = {r[k], u[k], v[k], w[k], th[k]};
+            double pr[5];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                pr[f] = qv[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+                a.A[oo + f * fs] = qv[f] + dt * (a.a_a * (Rv[f] - Lv[f]) + a.at_a * Lv[f]);
+                a.F[oo + f * fs] = qv[f] + a.cb * Rv[f];
+            }
+            a.P[oo] = pr[0];
+            a.P[oo + 3 * fs] = pr[3];
+            a.P[oo + 4 * fs] = pr[4];
+            a.Quv[oo + fs] = bx ? 0.0 : pr[1];
+            a.Quv[oo + 2 * fs] = by ? 0.0 : pr[2];
+        } else if (MODE == M_S2) {
+            const double dt = a.dt;
+            double pr[5];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                pr[f] = Ain[k][f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+                a.F[oo + f * fs] = Fin[k][f] + a.cb * Rv[f];
+            }
+            a.P[oo] = pr[0];
+            a.P[oo + 3 * fs] = pr[3];
+            a.P[oo + 4 * fs] = pr[4];
+            a.Quv[oo + fs] = bx ? 0.0 : pr[1];
+            a.Quv[oo + 2 * fs] = by ? 0.0 : pr[2];
+        } else {
+            bool fin = true;
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                const double val = Fin[k][f] + a.cb * Rv[f];
+                fin = fin && isfinite(val);
+                a.out[oo + f * fs] = val;
+            }
+            if (!fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
         }
-        if (!fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
     }
 }
 
@@ -350,8 +395,8 @@ __device__ __forceinline__ void stage_manual(double* STG, const EArgs& a, int tx
     }
 }
 
-template <int N, int NY, int TX, int TY, int MODE>
-__global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, 1)
+template <int N, int NY, int TX, int TY, int MODE, int MINB>
+__global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     k_explicit2(const EArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T = E2<N, NY, TX, TY>;
     constexpr int PL = T::PL, LXT = T::LXT, NL = T::NL, BLK = T::BLK;
@@ -419,22 +464,25 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, 1)
         __syncthreads();
     }
 
-    // ---- the thread's main point (fixed for the whole sweep) --------------
+    // ---- the thread's main points (fixed for the whole sweep) -------------
+    constexpr int K = T::K;
     const bool has_main = tid < T::NT;
     const int mox = tid % T::OX;
-    const int moz = (tid / T::OX) % N;
-    const int moy = tid / (T::OX * N);
+    const int mop = (tid / T::OX) % (N / K);
+    const int moy = tid / (T::OX * (N / K));
+    const int moz = mop * K;
     const bool main_ok = has_main && mox < oxm && moy < oym;
     const int mgx = ex0 * N + mox, mgy = ey0 * NY + moy;
     const PAx max_ = pax(mgx, mox + N, N, g.nex);
     const PAx may_ = pax(mgy, moy + NY, NY, g.ney);
-    DRows<N, NY> Dm;
+    DRows<N, NY, K> Dm;
     double mcx = 0.0, mcy = 0.0;
     if (main_ok) {
 #pragma unroll
         for (int m = 0; m <= N; ++m) {
             Dm.x[m] = sDx[max_.row * (N + 1) + m];
-            Dm.z[m] = sDx[moz * (N + 1) + m];
+#pragma unroll
+            for (int k = 0; k < K; ++k) Dm.z[k][m] = sDx[(moz + k) * (N + 1) + m];
         }
 #pragma unroll
         for (int m = 0; m <= NY; ++m) Dm.y[m] = sDy[may_.row * (NY + 1) + m];
@@ -505,28 +553,12 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, 1)
                 for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sx[m], s);
                 XF[it] = s;
             }
-            // row N of this layer at its top face: carry into the next layer
-            if (ez + 1 < g.nez) {
-                const int ncol = oxn * oyn;
-                for (int it = tid; it < 7 * ncol; it += BLK) {
-                    const int c = it % ncol;
-                    const int f = it / ncol;
-                    if ((f == 6 && !NEED_L) || (f == 5 && !NEED_R)) continue;
-                    const int ox = c % oxn, oy = c / oxn;
-                    const double* sz = S + f * (NL * PL) + (oy + NY) * LXT + (ox + N);
-                    double s = 0.0;
-#pragma unroll
-                    for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sz[((base + m) % NL) * PL], s);
-                    CARw[f * (T::CYW * T::CXW) + oy * T::CXW + ox] = s;
-                }
-            }
         }
         __syncthreads();
         // ---------------- 3. points ------------------------------------------
         if (main_ok) {
-            e2_point<N, NY, TX, TY, MODE, true>(a, S, CARr, XF, LT, Dm, sDx, sDy, max_, may_, moz,
-                                                mox, moy,
-                                                mgx, mgy, base + moz, ez, mcx, mcy, Z);
+            e2_pts<N, NY, TX, TY, MODE, true, K>(a, S, CARr, CARw, XF, LT, Dm, sDx, sDy, max_, may_,
+                                                 moz, mox, moy, mgx, mgy, ez, mcx, mcy, Z);
         }
         // points outside the main box: domain-end x column / y row, top level
         const int ozn = N + ((ez == g.nez - 1) ? 1 : 0);
@@ -542,17 +574,17 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, 1)
                 const PAx ax = pax(gx, ox + N, N, g.nex);
                 const PAx ay = pax(gy, oy + NY, NY, g.ney);
                 const PAx az = pax(gz, oz, N, g.nez);
-                DRows<N, NY> De;
+                DRows<N, NY, 1> De;
 #pragma unroll
                 for (int m = 0; m <= N; ++m) {
                     De.x[m] = sDx[ax.row * (N + 1) + m];
-                    De.z[m] = sDx[az.row * (N + 1) + m];
+                    De.z[0][m] = sDx[az.row * (N + 1) + m];
                 }
 #pragma unroll
                 for (int m = 0; m <= NY; ++m) De.y[m] = sDy[ay.row * (NY + 1) + m];
-                e2_point<N, NY, TX, TY, MODE, false>(a, S, CARr, XF, LT, De, sDx, sDy, ax, ay, oz,
-                                                     ox, oy, gx,
-                                                     gy, gz, ez, __ldg(a.cx + gx), __ldg(a.cy + gy), Z);
+                e2_pts<N, NY, TX, TY, MODE, false, 1>(a, S, CARr, CARw, XF, LT, De, sDx, sDy, ax, ay,
+                                                      oz, ox, oy, gx, gy, ez, __ldg(a.cx + gx),
+                                                      __ldg(a.cy + gy), Z);
             }
         }
         __syncthreads();

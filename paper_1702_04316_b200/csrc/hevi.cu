@@ -19,6 +19,12 @@
 //    (box meshes: all columns identical), extraction -- fused.
 #include "../../include/hevi.h"
 
+#ifndef HEVI_T44_TX
+#define HEVI_T44_TX 4
+#define HEVI_T44_TY 2
+#define HEVI_T44_MINB 1
+#endif
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -975,22 +981,22 @@ int dispatch_e(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
 // ---- v2 explicit dispatch (TMA ring-buffer kernel) ------------------------
 template <int N, int NY>
 struct Tile2 {
-    static constexpr int TX = 0, TY = 0;
+    static constexpr int TX = 0, TY = 0, MINB = 1;
 };
-template <> struct Tile2<1, 1> { static constexpr int TX = 16, TY = 16; };
-template <> struct Tile2<2, 2> { static constexpr int TX = 8, TY = 4; };
-template <> struct Tile2<3, 3> { static constexpr int TX = 4, TY = 2; };
-template <> struct Tile2<4, 4> { static constexpr int TX = 4, TY = 2; };
-template <> struct Tile2<5, 5> { static constexpr int TX = 2, TY = 2; };
-template <> struct Tile2<6, 6> { static constexpr int TX = 2, TY = 1; };
-template <> struct Tile2<7, 7> { static constexpr int TX = 1, TY = 1; };
-template <> struct Tile2<2, 1> { static constexpr int TX = 32, TY = 1; };
-template <> struct Tile2<3, 1> { static constexpr int TX = 16, TY = 1; };
-template <> struct Tile2<4, 1> { static constexpr int TX = 8, TY = 1; };
-template <> struct Tile2<5, 1> { static constexpr int TX = 8, TY = 1; };
-template <> struct Tile2<6, 1> { static constexpr int TX = 6, TY = 1; };
-template <> struct Tile2<7, 1> { static constexpr int TX = 4, TY = 1; };
-template <> struct Tile2<8, 1> { static constexpr int TX = 4, TY = 1; };
+template <> struct Tile2<1, 1> { static constexpr int TX = 16, TY = 16, MINB = 1; };
+template <> struct Tile2<2, 2> { static constexpr int TX = 8, TY = 4, MINB = 1; };
+template <> struct Tile2<3, 3> { static constexpr int TX = 4, TY = 2, MINB = 2; };
+template <> struct Tile2<4, 4> { static constexpr int TX = HEVI_T44_TX, TY = HEVI_T44_TY, MINB = HEVI_T44_MINB; };
+template <> struct Tile2<5, 5> { static constexpr int TX = 2, TY = 2, MINB = 1; };
+template <> struct Tile2<6, 6> { static constexpr int TX = 2, TY = 1, MINB = 1; };
+template <> struct Tile2<7, 7> { static constexpr int TX = 1, TY = 1, MINB = 1; };
+template <> struct Tile2<2, 1> { static constexpr int TX = 32, TY = 1, MINB = 2; };
+template <> struct Tile2<3, 1> { static constexpr int TX = 16, TY = 1, MINB = 2; };
+template <> struct Tile2<4, 1> { static constexpr int TX = 8, TY = 1, MINB = 2; };
+template <> struct Tile2<5, 1> { static constexpr int TX = 8, TY = 1, MINB = 1; };
+template <> struct Tile2<6, 1> { static constexpr int TX = 6, TY = 1, MINB = 1; };
+template <> struct Tile2<7, 1> { static constexpr int TX = 4, TY = 1, MINB = 1; };
+template <> struct Tile2<8, 1> { static constexpr int TX = 4, TY = 1, MINB = 1; };
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1037,7 +1043,7 @@ int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) 
         const Geo& g = pl->g;
         const size_t smem = T::fixed_bytes() + sizeof(double) * T::NTAB * g.Z;
         if (smem > 225 * 1024) return HEVI_OK;   // v1 handles it
-        auto kern = k_explicit2<N, NY, TX, TY, MODE>;
+        auto kern = k_explicit2<N, NY, TX, TY, MODE, Tile2<N, NY>::MINB>;
         static size_t attr = 0;
         if (attr < smem) {
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
