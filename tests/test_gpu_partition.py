@@ -1,0 +1,71 @@
+"""The column-partitioned step is bitwise the single-GPU step (SURVEY 8(c)
+gate C).  Ranks are emulated on one device in lock-step (LocalExchange)
+rather than as processes that wait on one another on one GPU."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1702_04316_b200 import specgrid, euler, imexcore, cases  # noqa: E402
+from paper_1702_04316_b200 import distributed as dd  # noqa: E402
+from paper_1702_04316_b200.stepper import HeviStepper  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def setup():
+    mesh = specgrid.build_box_mesh_3d(8, 6, 3, 32_000.0, 24_000.0, 300.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    q0 = cases.bubble_lattice(mesh, ref, 0.5, (16_000.0, 12_000.0, 150.0), (6000.0, 6000.0, 100.0))
+    dt = cases.dt_for_courant(mesh, ref, q0, 15.0)
+    return mesh, ref, disc, q0, dt
+
+
+def single(setup, nsteps):
+    mesh, ref, disc, q0, dt = setup
+    st = HeviStepper(disc, ref, dt)
+    st.set_state(q0, lattice=True)
+    st.step(nsteps)
+    return st.state(lattice=True).clone()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_partitioned_step_is_bitwise_single_gpu(setup, world):
+    mesh, ref, disc, q0, dt = setup
+    want = single(setup, 2)
+    px, py = dd.grid_for(world)
+    ex = dd.LocalExchange(mesh, px, py)
+    steppers = [dd.DistributedStepper(mesh, ref, disc, dt, px, py, r, exchange=ex)
+                for r in range(world)]
+    for s in steppers:
+        s.load_global(q0)
+    dd.run_local_partitioned(steppers, ex, nsteps=2)
+    torch.cuda.synchronize()
+    for s in steppers:
+        s.plan.check_flags()
+        x0, x1, y0, y1 = s.owned_region()
+        got = s.owned()[..., :x1 - x0]
+        assert torch.equal(got, want[:, :, y0:y1, x0:x1]), (world, s.block.rank)
+
+
+def test_stepper_graph_replay_matches_eager(setup):
+    mesh, ref, disc, q0, dt = setup
+    want = single(setup, 3)
+    st = HeviStepper(disc, ref, dt)
+    st.set_state(q0, lattice=True)
+    st.capture()          # records (and runs) one step
+    st.step(2)
+    assert torch.equal(st.state(lattice=True), want)
+
+
+def test_resident_stepper_matches_drop_in_step(setup):
+    mesh, ref, disc, q0, dt = setup
+    plan = disc.plan_for(ref)
+    E = plan.l2e(q0)
+    prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+                                    solver=imexcore.SolverSpec(method="direct"))
+    out = imexcore.ark_imex_step(E, dt, imexcore.ark2_tableau(), prob,
+                                 euler.make_rhs(ref, disc, "set2nc"))
+    want = single(setup, 1)
+    assert torch.equal(plan.e2l(out)[..., :mesh.X], want)
