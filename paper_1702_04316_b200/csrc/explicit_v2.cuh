@@ -42,7 +42,7 @@ struct E2 {
     static constexpr int BLK = (NT + 31) / 32 * 32;
     static constexpr int CXW = OX + 1, CYW = TY * NY + 1 + (NY == 1 ? 1 : 0);
     static constexpr int STG_N = 5 * NL * PL;                 // TMA staging
-    static constexpr int S_N = 7 * NL * PL;                   // ring of 7 fields
+    static constexpr int S_N = 6 * NL * PL;                   // ring: rho', u, v, w, theta', P'
     static constexpr int CAR_N = 2 * 7 * CYW * CXW;           // double-buffered carry
     static constexpr int XF_N = 6 * TX * OYM * N;             // x-face partials
     static constexpr int DN = (N + 1) * (N + 1), DNY = (NY + 1) * (NY + 1);
@@ -228,10 +228,19 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                 gyv[k] = cy * e;
             }
         }
-        const double* sz = Sf + ay.l * LXT + ax.l;
         double val[N + 1];
+        if (f == 6) {
+            // linearised pressure G0 rho' + H0 theta' (euler.py:188-194) on the z-line
+            const double* s0 = S + ay.l * LXT + ax.l;
+            const double* s4 = S + 4 * (NL * PL) + ay.l * LXT + ax.l;
 #pragma unroll
-        for (int m = 0; m <= N; ++m) val[m] = sz[zs[m]];
+            for (int m = 0; m <= N; ++m)
+                val[m] = LT[T_G0 * Z + base + m] * s0[zs[m]] + LT[T_H0 * Z + base + m] * s4[zs[m]];
+        } else {
+            const double* sz = Sf + ay.l * LXT + ax.l;
+#pragma unroll
+            for (int m = 0; m <= N; ++m) val[m] = sz[zs[m]];
+        }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             double d = 0.0;
@@ -507,11 +516,10 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
             const double r = STG[0 * NL * PL + st], u = STG[1 * NL * PL + st],
                          v = STG[2 * NL * PL + st], w = STG[3 * NL * PL + st],
                          th = STG[4 * NL * PL + st];
-            double pp = 0.0, pl = 0.0;
+            double pp = 0.0;
             if (NEED_R)
                 pp = pprime(r, th, LT[T_RHO0 * Z + gz], LT[T_TH0 * Z + gz], LT[T_E0 * Z + gz],
                             LT[T_C0 * Z + gz], LT[T_IRT0 * Z + gz], LT[T_P0F * Z + gz], bc, a.ph);
-            if (NEED_L) pl = LT[T_G0 * Z + gz] * r + LT[T_H0 * Z + gz] * th;
             const int d = ((gz % NL) * T::LY + ly) * LXT + lx;
             S[0 * NL * PL + d] = r;
             S[1 * NL * PL + d] = u;
@@ -519,7 +527,6 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
             S[3 * NL * PL + d] = w;
             S[4 * NL * PL + d] = th;
             S[5 * NL * PL + d] = pp;
-            S[6 * NL * PL + d] = pl;
         }
         __syncthreads();
         // the staging buffer is free: fetch the next layer under this layer's compute

@@ -21,7 +21,11 @@
 
 #ifndef HEVI_T44_TX
 #define HEVI_T44_TX 4
+#endif
+#ifndef HEVI_T44_TY
 #define HEVI_T44_TY 2
+#endif
+#ifndef HEVI_T44_MINB
 #define HEVI_T44_MINB 1
 #endif
 
@@ -873,6 +877,7 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 }
 
 #include "explicit_v2.cuh"
+#include "explicit_v3.cuh"
 #include "solve_v2.cuh"
 
 }  // namespace
@@ -905,6 +910,7 @@ struct hevi_plan {
     std::map<long long, Factor> factors;
     double bc[16];
     bool use_v2 = true;
+    bool use_v3 = false;
     bool use_tma = true;
 };
 
@@ -1032,8 +1038,46 @@ int make_tmap(CUtensorMap* m, const Geo& g, const double* base, int bx, int by, 
     return HEVI_OK;
 }
 
+template <int N, int NY>
+struct Tile3 {
+    static constexpr int TX = 0, TY = 0;
+};
+template <> struct Tile3<4, 4> { static constexpr int TX = 4, TY = 2; };
+
+template <int N, int NY, int MODE>
+int launch_e3(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) {
+    constexpr int TX = Tile3<N, NY>::TX, TY = Tile3<N, NY>::TY;
+    done = false;
+    if constexpr (TX == 0) {
+        return HEVI_OK;
+    } else {
+        using T = E3<N, NY, TX, TY>;
+        const Geo& g = pl->g;
+        const size_t smem = T::fixed_bytes() + sizeof(double) * T::NTAB * g.Z;
+        if (smem > 225 * 1024) return HEVI_OK;
+        auto kern = k_explicit3<N, NY, TX, TY, MODE>;
+        static size_t attr = 0;
+        if (attr < smem) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = smem;
+        }
+        CUtensorMap tm;
+        int rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, T::NL);
+        if (rc) return rc;
+        dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
+        kern<<<grid, T::BLK, smem, st>>>(a, tm);
+        CK(cudaGetLastError());
+        done = true;
+        return HEVI_OK;
+    }
+}
+
 template <int N, int NY, int MODE>
 int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) {
+    if (pl->use_v3) {
+        int rc = launch_e3<N, NY, MODE>(pl, a, st, done);
+        if (rc || done) return rc;
+    }
     constexpr int TX = Tile2<N, NY>::TX, TY = Tile2<N, NY>::TY;
     done = false;
     if constexpr (TX == 0) {
@@ -1361,6 +1405,7 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     }
     pl->use_v2 = getenv("HEVI_KERNELS") == nullptr || strcmp(getenv("HEVI_KERNELS"), "v1") != 0;
     pl->use_tma = getenv("HEVI_NO_TMA") == nullptr;
+    pl->use_v3 = getenv("HEVI_KERNELS") != nullptr && strcmp(getenv("HEVI_KERNELS"), "v3") == 0;
     *out = pl;
     return HEVI_OK;
 }
