@@ -104,6 +104,11 @@ int hevi_stage_solve(hevi_plan *plan, int stage, double lam, double *work, void 
 int hevi_ark2_step(hevi_plan *plan, double dt, const double *tab, double *Q, double *work,
                    void *stream);
 
+/* imexcore.rk35_step (imexcore.py:111-126): SSP RK(5,3) explicit step,
+ * Q <- step(Q); work = 4 lattice arrays.  The explicit reference the HEVI
+ * step is compared with (BASELINE config 2). */
+int hevi_rk35_step(hevi_plan *plan, double dt, double *Q, double *work, void *stream);
+
 /* E-vector <-> lattice (exact for DSS-continuous fields; the lattice takes
  * the first-occurrence copy, columnsolve.unique_space rep :28-34) */
 int hevi_evec_to_lattice(hevi_plan *plan, const double *E, double *Lat, int nfields, void *stream);

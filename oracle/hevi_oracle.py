@@ -504,6 +504,29 @@ class BoxOracle:
             raise FloatingPointError("non-finite state after IMEX step")
         return out
 
+    # -- SSP RK(5,3) explicit step (imexcore.py:79-126) -----------------------
+    _RK_A = {(1, 0): 1.0, (2, 1): 1.0, (3, 0): 0.355909775063327, (3, 2): 0.644090224936674,
+             (4, 0): 0.367933791638137, (4, 3): 0.632066208361863,
+             (5, 2): 0.237593836598569, (5, 4): 0.762406163401431}
+    _RK_B = {(1, 0): 0.377268915331368, (2, 1): 0.377268915331368, (3, 2): 0.242995220537396,
+             (4, 3): 0.238458932846290, (5, 4): 0.287632146308408}
+
+    def rk35(self, q, dt):
+        u = [q]
+        for i in range(1, 6):
+            acc = np.zeros_like(q)
+            for j in range(i):
+                al = self._RK_A.get((i, j), 0.0)
+                be = self._RK_B.get((i, j), 0.0)
+                if al != 0.0:
+                    acc += al * u[j]
+                if be != 0.0:
+                    acc += (be * dt) * self.rhs(u[j])
+            u.append(acc)
+        if np.any(~np.isfinite(u[5])):
+            raise FloatingPointError("non-finite state in explicit stage")
+        return u[5]
+
     # -- helpers -------------------------------------------------------------
     def min_node_spacing(self):
         """euler.min_node_spacing (euler.py:583-593)."""

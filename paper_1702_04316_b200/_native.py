@@ -60,6 +60,7 @@ SIGNATURES = {
     "hevi_stage": (_I, [_V, _I, _D, _V, _V, _V, _V]),
     "hevi_stage_solve": (_I, [_V, _I, _D, _V, _V]),
     "hevi_ark2_step": (_I, [_V, _D, _V, _V, _V, _V]),
+    "hevi_rk35_step": (_I, [_V, _D, _V, _V, _V]),
     "hevi_evec_to_lattice": (_I, [_V, _V, _V, _I, _V]),
     "hevi_lattice_to_evec": (_I, [_V, _V, _V, _I, _V]),
     "hevi_flags": (_I, [_V, ctypes.POINTER(ctypes.c_uint), _I, _V]),

@@ -162,7 +162,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
     double Ain[K][5], Fin[K][5];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        if (MODE == M_S2) {
+        if (MODE == M_S2 || (MODE == M_RK && a.A != nullptr)) {
 #pragma unroll
             for (int f = 0; f < 5; ++f) Ain[k][f] = a.A[o[k] + f * fs];
         }
@@ -371,6 +371,19 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
             a.P[oo + 4 * fs] = pr[4];
             a.Quv[oo + fs] = bx ? 0.0 : pr[1];
             a.Quv[oo + 2 * fs] = by ? 0.0 : pr[2];
+        } else if (MODE == M_RK) {
+            // SSP RK(5,3) Shu-Osher stage (imexcore.py:111-126)
+            const double qv[5] = {r[k], u[k], v[k], w[k], th[k]};
+            bool fin = true;
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                double val = a.A ? a.a_p * Ain[k][f] : 0.0;
+                val = val + a.at_p * qv[f];
+                val = val + a.cb * Rv[f];
+                fin = fin && isfinite(val);
+                a.out[oo + f * fs] = val;
+            }
+            if (a.rk_final && !fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
         } else {
             bool fin = true;
 #pragma unroll

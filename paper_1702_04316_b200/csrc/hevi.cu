@@ -81,7 +81,9 @@ struct Phys {
     double g, R, P0, gamma;
 };
 
-enum { M_R = 0, M_L = 1, M_S1 = 2, M_S2 = 3, M_S3 = 4 };
+enum { M_R = 0, M_L = 1, M_S1 = 2, M_S2 = 3, M_S3 = 4, M_RK = 5 };
+// M_RK: one SSP RK(5,3) Shu-Osher stage (imexcore.py:111-126):
+//   out = a_p * A + at_p * q + cb * R(q)     (A may be null: no a_p term)
 
 struct EArgs {
     Geo g;
@@ -100,6 +102,7 @@ struct EArgs {
     int stage;
     double bc[16];   // binomial coefficients C(gamma, k), k = 1..15 (EOS series)
     int use_tma;     // 1: TMA staging (default); 0: cooperative loads
+    int rk_final;    // M_RK: last stage (non-finite output check, imexcore.py:124-125)
 };
 
 struct SArgs {
@@ -398,6 +401,19 @@ __global__ void __launch_bounds__(ETile<NX, NY, NZ, TX, TY>::BLK)
                 a.P[o + 4 * fs] = pr[4];
                 a.Quv[o + fs] = bx ? 0.0 : pr[1];
                 a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+            } else if (MODE == M_RK) {
+                const double Rv[5] = {R0, R1, R2, R3, R4};
+                const double qv[5] = {r, u, v, w, th};
+                bool fin = true;
+#pragma unroll
+                for (int f = 0; f < 5; ++f) {
+                    double val = a.A ? a.a_p * a.A[o + f * fs] : 0.0;
+                    val = val + a.at_p * qv[f];
+                    val = val + a.cb * Rv[f];
+                    fin = fin && isfinite(val);
+                    a.out[o + f * fs] = val;
+                }
+                if (a.rk_final && !fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
             } else {  // M_S3
                 const double Rv[5] = {R0, R1, R2, R3, R4};
                 bool fin = true;
@@ -1048,7 +1064,7 @@ template <int N, int NY, int MODE>
 int launch_e3(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) {
     constexpr int TX = Tile3<N, NY>::TX, TY = Tile3<N, NY>::TY;
     done = false;
-    if constexpr (TX == 0) {
+    if constexpr (TX == 0 || MODE == M_RK) {
         return HEVI_OK;
     } else {
         using T = E3<N, NY, TX, TY>;
@@ -1139,6 +1155,7 @@ int run_e2(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st, bool&
         case M_S1: return dispatch_e2<M_S1>(pl, a, st, done);
         case M_S2: return dispatch_e2<M_S2>(pl, a, st, done);
         case M_S3: return dispatch_e2<M_S3>(pl, a, st, done);
+        case M_RK: return dispatch_e2<M_RK>(pl, a, st, done);
     }
     return fail("bad mode");
 }
@@ -1155,6 +1172,7 @@ int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
         case M_S1: return dispatch_e<M_S1>(pl, a, st);
         case M_S2: return dispatch_e<M_S2>(pl, a, st);
         case M_S3: return dispatch_e<M_S3>(pl, a, st);
+        case M_RK: return dispatch_e<M_RK>(pl, a, st);
     }
     return fail("bad mode");
 }
@@ -1597,6 +1615,37 @@ int hevi_ark2_step(hevi_plan* pl, double dt, const double* tab, double* Q, doubl
     if ((rc = hevi_stage(pl, 1, dt, tab, Q, work, stream))) return rc;
     if ((rc = hevi_stage_solve(pl, 1, lam, work, stream))) return rc;
     return hevi_stage(pl, 2, dt, tab, Q, work, stream);
+}
+
+int hevi_rk35_step(hevi_plan* pl, double dt, double* Q, double* work, void* stream) {
+    if (!pl || !Q || !work) return fail("null argument");
+    // Shu-Osher coefficients of SSP RK(5,3) (imexcore.py:81-94): stage i combines
+    // alpha_a u_a (optional), alpha_b u_{i-1} and beta dt R(u_{i-1})
+    static const double al_a[5] = {0.0, 0.0, 0.355909775063327, 0.367933791638137,
+                                   0.237593836598569};
+    static const double al_b[5] = {1.0, 1.0, 0.644090224936674, 0.632066208361863,
+                                   0.762406163401431};
+    static const double be[5] = {0.377268915331368, 0.377268915331368, 0.242995220537396,
+                                 0.238458932846290, 0.287632146308408};
+    const long long fs5 = 5 * pl->g.fs;
+    double* W[4] = {work, work + fs5, work + 2 * fs5, work + 3 * fs5};
+    double* qin[5] = {Q, W[0], W[1], W[2], W[3]};
+    double* xin[5] = {nullptr, nullptr, Q, Q, W[1]};
+    double* out[5] = {W[0], W[1], W[2], W[3], Q};
+    for (int i = 0; i < 5; ++i) {
+        EArgs a = base_eargs(pl);
+        a.q = qin[i];
+        a.A = xin[i];
+        a.out = out[i];
+        a.a_p = al_a[i];
+        a.at_p = al_b[i];
+        a.cb = be[i] * dt;
+        a.stage = i < 2 ? i : 2;
+        a.rk_final = (i == 4);
+        int rc = run_e(pl, M_RK, a, (cudaStream_t)stream);
+        if (rc) return rc;
+    }
+    return HEVI_OK;
 }
 
 int hevi_evec_to_lattice(hevi_plan* pl, const double* E, double* Lt, int nf, void* stream) {

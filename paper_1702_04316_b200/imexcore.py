@@ -52,6 +52,66 @@ def ark2_tableau() -> ButcherPair:
     return ButcherPair(a=a, at=at, b=b, c=a.sum(axis=1), ct=at.sum(axis=1))
 
 
+# Shu-Osher representation of SSP RK(5,3) (imexcore.py:79-94)
+_RK35_ALPHA = {
+    (1, 0): 1.0,
+    (2, 1): 1.0,
+    (3, 0): 0.355909775063327, (3, 2): 0.644090224936674,
+    (4, 0): 0.367933791638137, (4, 3): 0.632066208361863,
+    (5, 2): 0.237593836598569, (5, 4): 0.762406163401431,
+}
+_RK35_BETA = {
+    (1, 0): 0.377268915331368,
+    (2, 1): 0.377268915331368,
+    (3, 2): 0.242995220537396,
+    (4, 3): 0.238458932846290,
+    (5, 4): 0.287632146308408,
+}
+
+
+def rk35_butcher():
+    """Butcher (A, b, c) of the SSP RK(5,3) scheme (imexcore.py:97-108)."""
+    rows = [np.zeros(5)]
+    for i in range(1, 6):
+        row = np.zeros(5)
+        for j in range(i):
+            row += _RK35_ALPHA.get((i, j), 0.0) * rows[j]
+            row[j] += _RK35_BETA.get((i, j), 0.0)
+        rows.append(row)
+    A = np.vstack(rows[:5])
+    return A, rows[5], A.sum(axis=1)
+
+
+def rk35_step(q, dt: float, rhs):
+    """One SSP RK(5,3) step (imexcore.py:111-126).  With ``rhs`` an
+    ``euler.RHS`` the five stages run as fused device launches."""
+    if isinstance(rhs, euler.RHS):
+        from .plan import to_device
+        plan = rhs.disc.plan_for(rhs.ref)
+        E, back = to_device(q)
+        Q = plan.e2l(E)
+        work = plan.workspace()
+        plan.rk35(dt, Q, work)
+        plan.check_flags()
+        return back(plan.l2e(Q))
+    u = [q]
+    for i in range(1, 6):
+        acc = q * 0.0
+        for j in range(i):
+            al = _RK35_ALPHA.get((i, j), 0.0)
+            be = _RK35_BETA.get((i, j), 0.0)
+            if al != 0.0:
+                acc += al * u[j]
+            if be != 0.0:
+                acc += (be * dt) * rhs(u[j])
+        u.append(acc)
+    out = u[5]
+    finite = np.isfinite(out).all() if isinstance(out, np.ndarray) else bool(out.isfinite().all())
+    if not finite:
+        raise FloatingPointError("non-finite state in explicit stage")
+    return out
+
+
 @dataclass
 class SolverSpec:
     """imexcore.py:133-140 (only method='direct' is on the HEVI path)."""

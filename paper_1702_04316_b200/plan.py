@@ -147,6 +147,9 @@ class HeviPlan:
         nv.check(self.lib.hevi_ark2_step(self.h, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
                                          nv.stream_ptr()))
 
+    def rk35(self, dt, Q, work):
+        nv.check(self.lib.hevi_rk35_step(self.h, float(dt), nv.ptr(Q), nv.ptr(work), nv.stream_ptr()))
+
     def stage(self, s, dt, tab: np.ndarray, Q, work):
         nv.check(self.lib.hevi_stage(self.h, s, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
                                      nv.stream_ptr()))

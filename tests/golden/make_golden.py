@@ -200,6 +200,24 @@ def run_case(name, mesh, N_s, slab, ops_seed, lam, bubble, C, nsteps, keep,
     print(name, {k: v.shape for k, v in out.items()}, "dt", dt)
 
 
+def run_rk35_case(name, mesh, N_s, slab, bubble, C, nsteps, keep):
+    """Explicit SSP RK(5,3) reference trajectory (imexcore.rk35_step)."""
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rep, dims, _ = lattice_index(mesh, N_s)
+    L = lambda f: to_lattice(f, rep, dims)  # noqa: E731
+    q = bubble_state(mesh, ref, disc, *bubble, slab=slab)
+    dt = dt_for(mesh, ref, disc, q, C)
+    out = {"step_q0": L(q), "step_dt": np.array(dt)}
+    rhs = lambda s: euler.nonlinear_rhs(s, ref, disc, "set2nc")  # noqa: E731
+    for k in range(1, nsteps + 1):
+        q = imx.rk35_step(q, dt, rhs)
+        if k in keep:
+            out[f"step_q{k}"] = L(q)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "dt", dt)
+
+
 def main():
     host = {"numpy": np.__version__, "python": platform.python_version(),
             "machine": platform.machine(), "processor": platform.processor()}
@@ -236,6 +254,11 @@ def main():
     run_case("straka_n7", mesh, 1, True, ops_seed=3, lam=0.5,
              bubble=(-15.0, (25_600.0, 0.0, 3_000.0), (4_000.0, 1.0, 2_000.0)),
              C=0.7, nsteps=5, keep=(1, 5))
+    # 5. explicit SSP RK(5,3) at C=1 on the 3D box (BASELINE config 2's explicit run)
+    mesh = box3d_mesh(4, 4, 4, 16_000.0, 16_000.0, 400.0, 4)
+    run_rk35_case("rk35_box3d_n4", mesh, 4, False,
+                  bubble=(0.5, (8_000.0, 8_000.0, 200.0), (4000.0, 4000.0, 100.0)),
+                  C=1.0, nsteps=10, keep=(1, 10))
     with open(os.path.join(HERE, "HOST.json"), "w") as f:
         json.dump(host, f, indent=1)
 

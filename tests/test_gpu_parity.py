@@ -171,3 +171,37 @@ def test_oracle_agrees_with_gpu_on_fresh_random_state(case):
                                     solver=imexcore.SolverSpec(method="direct"), lam=lam)
     S = prob.solve(dev(q)).cpu().numpy()
     assert max(rel_fields(o.to_lattice(S), o.to_lattice(o.solve(q, lam)))) < SOLVE_TOL
+
+
+def test_rk35_matches_reference():
+    """Device SSP RK(5,3) (5 fused R+combination launches) against the
+    reference explicit trajectory at C=1 (BASELINE config 2's explicit run)."""
+    from conftest import load_golden
+    from oracle.hevi_oracle import BoxOracle
+    g = load_golden("rk35_box3d_n4")
+    o = BoxOracle(4, 4, 4, 16_000.0, 16_000.0, 400.0, 4)
+    mesh = specgrid.build_box_mesh_3d(4, 4, 4, 16_000.0, 16_000.0, 400.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rhs = euler.make_rhs(ref, disc, "set2nc")
+    q = dev(o.from_lattice(g["step_q0"]))
+    dt = float(g["step_dt"])
+    generic = imexcore.rk35_step(q, dt, lambda s: euler.nonlinear_rhs(s, ref, disc, "set2nc"))
+    for k in range(1, 11):
+        q = imexcore.rk35_step(q, dt, rhs)
+        if k == 1:
+            assert max(rel_fields(q.cpu().numpy(), generic.cpu().numpy())) < 1e-13
+        if k in (1, 10):
+            e_rho, e_vel, e_th = rel_fields(o.to_lattice(q.cpu().numpy()), g[f"step_q{k}"])
+            assert e_rho < STEP_SCALAR_TOL and e_th < STEP_SCALAR_TOL, (k, e_rho, e_th)
+            assert e_vel < STEP_VEL_TOL, (k, e_vel)
+
+
+def test_rk35_nan_detection():
+    mesh = specgrid.build_box_mesh_3d(2, 2, 2, 8000.0, 8000.0, 200.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    q = np.zeros((5,) + mesh.nshape)
+    q[3, 1, 2, 2, 2] = np.nan
+    with pytest.raises(FloatingPointError):
+        imexcore.rk35_step(q, 0.1, euler.make_rhs(ref, disc, "set2nc"))

@@ -282,3 +282,24 @@ def test_halo_plan_is_symmetric(world):
                 back = [t for t in plans[peer][ph] if t[0] == r]
                 assert len(back) == 1
                 assert back[0][1] == rreg and back[0][2] == sreg
+
+
+def test_rk35_butcher_order_conditions():
+    """test_imexcore.py:43-50."""
+    a, b, c = imexcore.rk35_butcher()
+    assert abs(b.sum() - 1.0) < 1e-13
+    assert abs(b @ c - 0.5) < 1e-13
+    assert abs(b @ c ** 2 - 1.0 / 3.0) < 1e-13
+    assert abs(b @ (a @ c) - 1.0 / 6.0) < 1e-13
+
+
+def test_rk35_generic_third_order_and_nan():
+    def err(dt):
+        q, t = np.array([1.0]), 0.0
+        while t < 1.0 - 1e-12:
+            q = imexcore.rk35_step(q, dt, lambda x: -x)
+            t += dt
+        return abs(q[0] - np.exp(-1.0))
+    assert 2.7 < math.log2(err(0.1) / err(0.05)) < 3.3
+    with pytest.raises(FloatingPointError):
+        imexcore.rk35_step(np.array([1.0]), 1.0, lambda x: x * np.nan)

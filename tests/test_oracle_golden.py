@@ -45,3 +45,17 @@ def test_oracle_steps_match_reference(case):
         if k in keep:
             errs = rel_fields(o.to_lattice(q), g[f"step_q{k}"])
             assert max(errs) < STEP_TOL, (name, k, errs)
+
+
+def test_oracle_rk35_matches_reference():
+    """Explicit SSP RK(5,3) trajectory (imexcore.py:111-126), C=1."""
+    from oracle.hevi_oracle import BoxOracle
+    g = load_golden("rk35_box3d_n4")
+    o = BoxOracle(4, 4, 4, 16_000.0, 16_000.0, 400.0, 4)
+    q = o.from_lattice(g["step_q0"])
+    dt = float(g["step_dt"])
+    for k in range(1, 11):
+        q = o.rk35(q, dt)
+        if k in (1, 10):
+            errs = rel_fields(o.to_lattice(q), g[f"step_q{k}"])
+            assert max(errs) < STEP_TOL, (k, errs)
