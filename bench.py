@@ -344,12 +344,18 @@ def run_gpu(args):
     kern = {}
     for n in names:
         avg = ktimes[n] / args.steps
+        if avg <= 0.0:
+            continue
         gbs = KERNEL_BYTES_PER_POINT[n] * pts_rank / (avg * 1e-3) / 1e9
         kern[n] = {"ms": round(avg, 4), "alg_bytes_per_point": KERNEL_BYTES_PER_POINT[n],
                    "alg_GBps": round(gbs, 1), "share": round(ktimes[n] / elapsed, 4)}
-    if rk:   # five R + Shu-Osher launches, each 2R(+1) 1W state passes
-        ktimes = {n: 0.0 for n in names}
-        ktimes["explicit_stage1"] = elapsed
+    if rk:   # whole RK35 step: 5 fused R + Shu-Osher launches (13 reads + 5 writes per point)
+        kern = {"rk35_step": {"ms": round(ms_step, 4), "alg_bytes_per_point": 8 * 5 * 18,
+                              "alg_GBps": round(8 * 5 * 18 * pts_rank / (ms_step * 1e-3) / 1e9, 1),
+                              "share": 1.0}}
+        KERNEL_BYTES_PER_POINT["rk35_step"] = 8 * 5 * 18
+        ktimes = {"rk35_step": elapsed}
+        names = ["rk35_step"]
     dom = max(names, key=lambda n: ktimes[n])
     traffic = None
     summ = ncu_traffic()
