@@ -188,25 +188,47 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
         v[k] = pp[2 * NL * PL];
         w[k] = pp[3 * NL * PL];
         th[k] = pp[4 * NL * PL];
-        rho[k] = LT[T_RHO0 * Z + gzk[k]] + r[k];
+        rho[k] = LT[gzk[k] * T::NTAB + T_RHO0] + r[k];
         rinv[k] = 1.0 / rho[k];
-        cz[k] = LT[T_CZ * Z + gzk[k]];
+        cz[k] = LT[gzk[k] * T::NTAB + T_CZ];
     }
     // d/dx, d/dy, d/dz of field f at the K points (DSS-averaged, folded)
+    // per-layer line base addresses: every line load below is base + a
+    // compile-time offset (field * SF + m * stride)
+    constexpr int SF = NL * PL;
+    const double* bx_[K];
+    const double* bxl_[K];
+    const double* by_[K];
+    const double* byl_[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        bx_[k] = S + sl[k] * PL + ay.l * LXT + ax.s0;
+        bxl_[k] = S + sl[k] * PL + ay.l * LXT + ax.l - N;
+        by_[k] = S + sl[k] * PL + ay.s0 * LXT + ax.l;
+        byl_[k] = S + sl[k] * PL + (ay.l - NY) * LXT + ax.l;
+    }
+    const double* bz_[N + 1];
+#pragma unroll
+    for (int m = 0; m <= N; ++m) bz_[m] = S + zs[m] + ay.l * LXT + ax.l;
+    const double* xfp = XF + ((TX == 0 ? 0 : ox / N) * T::OYM + oy) * N + oz0;
+    const double* carp = CARp + cidx;
+    double* carw = CARw + cidx;
+    // d/dx, d/dy, d/dz of field f at the K points (DSS-averaged, folded)
     auto grad = [&](int f, bool want_xy, double (&gxv)[K], double (&gyv)[K], double (&gzv)[K]) {
-        const double* Sf = S + f * (NL * PL);
         if (want_xy) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const double* sx = Sf + sl[k] * PL + ay.l * LXT + ax.s0;
+                const double* sx = bx_[k] + f * SF;
                 double d = 0.0;
 #pragma unroll
                 for (int m = 0; m <= N; ++m) d = fma(D.x[m], sx[m], d);
-                if (ax.face) {
-                    if (MAIN) {
-                        d += XF[((f * TX + ox / N) * T::OYM + oy) * N + oz0 + k];
-                    } else {
-                        const double* sxl = Sf + sl[k] * PL + ay.l * LXT + ax.l - N;
+                if (MAIN) {
+                    // branch-free: the XF slot is in bounds for every main point
+                    const double xf = xfp[f * (TX * T::OYM * N) + k];
+                    d += ax.face ? xf : 0.0;
+                } else if (ax.face) {
+                    {
+                        const double* sxl = bxl_[k] + f * SF;
                         double e = 0.0;
 #pragma unroll
                         for (int m = 0; m <= N; ++m) e = fma(sDx[N * (N + 1) + m], sxl[m], e);
@@ -214,12 +236,12 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                     }
                 }
                 gxv[k] = cx * d;
-                const double* sy = Sf + sl[k] * PL + ay.s0 * LXT + ax.l;
+                const double* sy = by_[k] + f * SF;
                 double e = 0.0;
 #pragma unroll
                 for (int m = 0; m <= NY; ++m) e = fma(D.y[m], sy[m * LXT], e);
                 if (ay.face) {
-                    const double* syl = Sf + sl[k] * PL + (ay.l - NY) * LXT + ax.l;
+                    const double* syl = byl_[k] + f * SF;
                     double h = 0.0;
 #pragma unroll
                     for (int m = 0; m <= NY; ++m) h = fma(sDy[NY * (NY + 1) + m], syl[m * LXT], h);
@@ -231,29 +253,29 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
         double val[N + 1];
         if (f == 6) {
             // linearised pressure G0 rho' + H0 theta' (euler.py:188-194) on the z-line
-            const double* s0 = S + ay.l * LXT + ax.l;
-            const double* s4 = S + 4 * (NL * PL) + ay.l * LXT + ax.l;
 #pragma unroll
             for (int m = 0; m <= N; ++m)
-                val[m] = LT[T_G0 * Z + base + m] * s0[zs[m]] + LT[T_H0 * Z + base + m] * s4[zs[m]];
+                val[m] = LT[(base + m) * T::NTAB + T_G0] * bz_[m][0] + LT[(base + m) * T::NTAB + T_H0] * bz_[m][4 * SF];
         } else {
-            const double* sz = Sf + ay.l * LXT + ax.l;
 #pragma unroll
-            for (int m = 0; m <= N; ++m) val[m] = sz[zs[m]];
+            for (int m = 0; m <= N; ++m) val[m] = bz_[m][f * SF];
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             double d = 0.0;
 #pragma unroll
             for (int m = 0; m <= N; ++m) d = fma(D.z[k][m], val[m], d);
-            if (k == 0 && zface) d += CARp[f * (T::CYW * T::CXW) + cidx];
+            if (k == 0) {
+                const double cr = carp[f * (T::CYW * T::CXW)];
+                d += zface ? cr : 0.0;
+            }
             gzv[k] = cz[k] * d;
         }
         if (do_carry) {
             double top = 0.0;
 #pragma unroll
             for (int m = 0; m <= N; ++m) top = fma(sDx[N * (N + 1) + m], val[m], top);
-            CARw[f * (T::CYW * T::CXW) + cidx] = top;
+            carw[f * (T::CYW * T::CXW)] = top;
         }
     };
     double R0[K], R1[K], R2[K], R3[K], R4[K], dwz[K], dPLz[K];
@@ -309,12 +331,12 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int gz = gzk[k];
-        const double drho0 = LT[T_DRHO0 * Z + gz];
-        const double dth0 = LT[T_DTH0 * Z + gz];
+        const double drho0 = LT[(gz) * T::NTAB + T_DRHO0];
+        const double dth0 = LT[(gz) * T::NTAB + T_DTH0];
         const bool bz = (gz == 0) || (gz == g.Z - 1);
         double Rv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         if (NEED_R) {
-            const double theta = LT[T_TH0 * Z + gz] + th[k];
+            const double theta = LT[(gz) * T::NTAB + T_TH0] + th[k];
             if (!(isfinite(r[k]) && isfinite(u[k]) && isfinite(v[k]) && isfinite(w[k]) &&
                   isfinite(th[k])))
                 atomicOr(a.flags, HEVI_F_NONFINITE_IN(a.stage));
@@ -330,8 +352,8 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
         double Lv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         if (NEED_L) {
             // euler.linear_operator(vertical_only=True), set2nc (euler.py:333-361)
-            const double irho0 = LT[T_IRHO0 * Z + gz];
-            Lv[0] = -(w[k] * drho0 + LT[T_RHO0 * Z + gz] * dwz[k]);
+            const double irho0 = LT[(gz) * T::NTAB + T_IRHO0];
+            Lv[0] = -(w[k] * drho0 + LT[(gz) * T::NTAB + T_RHO0] * dwz[k]);
             Lv[3] = bz ? 0.0 : -(dPLz[k] * irho0 + (r[k] * irho0) * gr);
             Lv[4] = -(w[k] * dth0);
         }
@@ -457,18 +479,18 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     for (int i = tid; i < T::DN; i += BLK) sDx[i] = a.Dx[i];
     for (int i = tid; i < T::DNY; i += BLK) sDy[i] = a.Dy[i];
     for (int k = tid; k < Z; k += BLK) {
-        LT[T_RHO0 * Z + k] = a.lv.rho0[k];
-        LT[T_TH0 * Z + k] = a.lv.theta0[k];
-        LT[T_E0 * Z + k] = a.lv.E0[k];
-        LT[T_C0 * Z + k] = a.lv.c0[k];
-        LT[T_IRT0 * Z + k] = a.lv.irt0[k];
-        LT[T_G0 * Z + k] = a.lv.G0[k];
-        LT[T_H0 * Z + k] = a.lv.H0[k];
-        LT[T_DRHO0 * Z + k] = a.lv.drho0[k];
-        LT[T_DTH0 * Z + k] = a.lv.dth0[k];
-        LT[T_CZ * Z + k] = a.cz[k];
-        LT[T_P0F * Z + k] = a.lv.P0f[k];
-        LT[T_IRHO0 * Z + k] = 1.0 / a.lv.rho0[k];
+        LT[(k) * T::NTAB + T_RHO0] = a.lv.rho0[k];
+        LT[(k) * T::NTAB + T_TH0] = a.lv.theta0[k];
+        LT[(k) * T::NTAB + T_E0] = a.lv.E0[k];
+        LT[(k) * T::NTAB + T_C0] = a.lv.c0[k];
+        LT[(k) * T::NTAB + T_IRT0] = a.lv.irt0[k];
+        LT[(k) * T::NTAB + T_G0] = a.lv.G0[k];
+        LT[(k) * T::NTAB + T_H0] = a.lv.H0[k];
+        LT[(k) * T::NTAB + T_DRHO0] = a.lv.drho0[k];
+        LT[(k) * T::NTAB + T_DTH0] = a.lv.dth0[k];
+        LT[(k) * T::NTAB + T_CZ] = a.cz[k];
+        LT[(k) * T::NTAB + T_P0F] = a.lv.P0f[k];
+        LT[(k) * T::NTAB + T_IRHO0] = 1.0 / a.lv.rho0[k];
     }
     __syncthreads();
     // window-local TMA coordinates of the tile origin
@@ -531,8 +553,8 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                          th = STG[4 * NL * PL + st];
             double pp = 0.0;
             if (NEED_R)
-                pp = pprime(r, th, LT[T_RHO0 * Z + gz], LT[T_TH0 * Z + gz], LT[T_E0 * Z + gz],
-                            LT[T_C0 * Z + gz], LT[T_IRT0 * Z + gz], LT[T_P0F * Z + gz], bc, a.ph);
+                pp = pprime(r, th, LT[(gz) * T::NTAB + T_RHO0], LT[(gz) * T::NTAB + T_TH0], LT[(gz) * T::NTAB + T_E0],
+                            LT[(gz) * T::NTAB + T_C0], LT[(gz) * T::NTAB + T_IRT0], LT[(gz) * T::NTAB + T_P0F], bc, a.ph);
             const int d = ((gz % NL) * T::LY + ly) * LXT + lx;
             S[0 * NL * PL + d] = r;
             S[1 * NL * PL + d] = u;
