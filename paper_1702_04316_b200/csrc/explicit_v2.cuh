@@ -535,10 +535,19 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     }
     const double* bc = a.bc;
 
+    // HEVI_PHASE_TIMING debug builds: per-phase clock64 sums (tools/phase_timing.py)
+#ifdef HEVI_PHASE_TIMING
+    unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long t0 = clock64(), t1;
+#define PH(i) do { t1 = clock64(); tph[i] += t1 - t0; t0 = t1; } while (0)
+#else
+#define PH(i) do { } while (0)
+#endif
     for (int ez = 0; ez < g.nez; ++ez) {
         const int base = ez * N;
         // ---------------- 1. staged layer -> ring slots ---------------------
         if (use_tma) mbar_wait(&mbar, ez & 1);
+        PH(0);
         const int lz0 = (ez == 0) ? 0 : 1;
         const int nconv = (NL - lz0) * T::LY * T::LX;
         for (int idx = tid; idx < nconv; idx += BLK) {
@@ -563,7 +572,9 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
             S[4 * NL * PL + d] = th;
             S[5 * NL * PL + d] = pp;
         }
+        PH(1);
         __syncthreads();
+        PH(2);
         // the staging buffer is free: fetch the next layer under this layer's compute
         if (use_tma) {
             if (tid == 0 && ez + 1 < g.nez) {
@@ -596,7 +607,9 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                 XF[it] = s;
             }
         }
+        PH(3);
         __syncthreads();
+        PH(4);
         // ---------------- 3. points ------------------------------------------
         if (main_ok) {
             e2_pts<N, NY, TX, TY, MODE, true, K>(a, S, CARr, CARw, XF, LT, Dm, sDx, sDy, max_, may_,
@@ -629,6 +642,15 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                                                       __ldg(a.cy + gy), Z);
             }
         }
+        PH(5);
         __syncthreads();
+        PH(6);
     }
+#ifdef HEVI_PHASE_TIMING
+    if (a.dbg) {
+        for (int i = 0; i < 7; ++i) atomicAdd(a.dbg + i, tph[i]);
+        atomicAdd(a.dbg + 7, 1ull);
+    }
+#endif
+#undef PH
 }

@@ -103,6 +103,7 @@ struct EArgs {
     double bc[16];   // binomial coefficients C(gamma, k), k = 1..15 (EOS series)
     int use_tma;     // 1: TMA staging (default); 0: cooperative loads
     int rk_final;    // M_RK: last stage (non-finite output check, imexcore.py:124-125)
+    unsigned long long* dbg;   // HEVI_PHASE_TIMING builds: per-phase clock64 sums
 };
 
 struct SArgs {
@@ -925,6 +926,7 @@ struct hevi_plan {
     unsigned* h_flags = nullptr;
     std::map<long long, Factor> factors;
     double bc[16];
+    unsigned long long* d_dbg = nullptr;
     bool use_v2 = true;
     bool use_v3 = false;
     bool use_tma = true;
@@ -1192,6 +1194,7 @@ EArgs base_eargs(const hevi_plan* pl) {
     a.flags = pl->d_flags;
     memcpy(a.bc, pl->bc, sizeof(a.bc));
     a.use_tma = pl->use_tma ? 1 : 0;
+    a.dbg = pl->d_dbg;
     return a;
 }
 
@@ -1339,6 +1342,16 @@ extern "C" {
 
 const char* hevi_last_error(void) { return g_err.c_str(); }
 
+#ifdef HEVI_PHASE_TIMING
+// debug builds only: per-phase clock64 sums of the explicit kernel, reset after read
+int hevi_debug_phase(hevi_plan* pl, unsigned long long* out8) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out8, pl->d_dbg, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(pl->d_dbg, 0, 8 * sizeof(unsigned long long)));
+    return HEVI_OK;
+}
+#endif
+
 int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_desc* rd) {
     if (!out || !gd || !rd) return fail("null argument");
     *out = nullptr;
@@ -1398,6 +1411,10 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     if (e == cudaSuccess) e = cudaMalloc(&pl->d_flags, 16 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(pl->d_flags, 0, 16 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMallocHost(&pl->h_flags, 16 * sizeof(unsigned));
+#ifdef HEVI_PHASE_TIMING
+    if (e == cudaSuccess) e = cudaMalloc(&pl->d_dbg, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(pl->d_dbg, 0, 8 * sizeof(unsigned long long));
+#endif
     if (e != cudaSuccess) {
         hevi_plan_destroy(pl);
         return fail("plan allocation", e);
