@@ -65,7 +65,9 @@ typedef struct {
                                P' = P - P0f evaluation (euler.py:454-457)      */
     const double *cx, *cy, *cz;
     const double *Dx, *Dy, *Dz;
+    const double *Theta0, *F0c; /* set2c: rho0 theta0 and gamma P0f / Theta0 (euler.py:103-113) */
     double g, R, P0, gamma;
+    int eqset;              /* 0: set2nc (rho', u, v, w, theta'); 1: set2c (rho', U, V, W, Theta') */
 } hevi_ref_desc;
 
 int hevi_plan_create(hevi_plan **plan, const hevi_grid_desc *grid, const hevi_ref_desc *ref);

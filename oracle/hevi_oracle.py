@@ -126,7 +126,20 @@ class BoxOracle:
     """
 
     def __init__(self, nx, ny, nz, Lx, Ly, Lz, N, slab=False,
-                 background="hydrostatic", theta_bg=300.0):
+                 background="hydrostatic", theta_bg=300.0, set_name="set2nc",
+                 pprime="reference"):
+        if set_name not in ("set2nc", "set2c"):
+            raise ValueError(set_name)
+        if pprime not in ("reference", "exact"):
+            raise ValueError(pprime)
+        self.set_name = set_name
+        # "reference": P' = eos(rho, theta) - P0f exactly as euler.py:456-457 /
+        # 479-480 (cancellation leaves ~eps*P0 ~ 1e-11 Pa of noise in P').
+        # "exact": the same P' evaluated without cancellation,
+        # Pb*expm1(gamma*log1p(delta)) + (Pb - P0f) with Pb = eos(rho0, theta0)
+        # and delta the relative perturbation of rho*theta -- the quantity the
+        # device series computes; a tighter checker for the kernels.
+        self.pprime = pprime
         if slab:
             ny = 1
             if Ly is None:
@@ -284,6 +297,9 @@ class BoxOracle:
         self.G0 = GAMMA * P0f / rho0
         self.H0 = GAMMA * P0f / theta0
         self.F0vec = self.G0[..., None] * self.grad_rho0 + self.H0[..., None] * self.grad_theta0
+        # set2c coefficients (euler.py:102-122)
+        self.Theta0 = rho0 * theta0
+        self.F0c = GAMMA * P0f / self.Theta0
 
     # -- pointwise pieces -----------------------------------------------------
     @staticmethod
@@ -292,6 +308,24 @@ class BoxOracle:
         if np.any(rho <= 0) or np.any(theta <= 0):
             raise ValueError("EOS requires positive density and temperature")
         return P_REF * (rho * R_GAS * theta / P_REF) ** GAMMA
+
+    def pprime_of(self, q):
+        """Perturbation pressure P' of the state q for the chosen set."""
+        rho = self.rho0 + q[0]
+        if self.set_name == "set2c":
+            theta = (self.Theta0 + q[4]) / rho
+        else:
+            theta = self.theta0 + q[4]
+        if self.pprime == "reference":
+            return self.eos(rho, theta) - self.P0f
+        self.eos(rho, theta)          # same positivity checks
+        rt0 = self.rho0 * self.theta0
+        if self.set_name == "set2c":
+            delta = q[4] / self.Theta0
+        else:
+            delta = (q[0] * self.theta0 + self.rho0 * q[4] + q[0] * q[4]) / rt0
+        Pb = self.eos(self.rho0, self.theta0)
+        return Pb * np.expm1(GAMMA * np.log1p(delta)) + (Pb - self.P0f)
 
     def grad(self, f):
         """specgrid.grad (specgrid.py:600-611)."""
@@ -322,10 +356,11 @@ class BoxOracle:
     def rhs(self, q):
         if np.any(~np.isfinite(q)):
             raise FloatingPointError("non-finite state passed to RHS evaluation")
+        if self.set_name == "set2c":
+            return self._rhs_c(q)
         u = np.moveaxis(q[1:4], 0, -1)
         rho = self.rho0 + q[0]
-        theta = self.theta0 + q[4]
-        Pp = self.eos(rho, theta) - self.P0f
+        Pp = self.pprime_of(q)
         divu = self.div(u)
 
         def advect(f, g0=None):
@@ -345,8 +380,29 @@ class BoxOracle:
         out[1:4] = self.no_flux(out[1:4])
         return out
 
-    # -- L_V(q): linear_operator(vertical_only=True), set2nc (euler.py:313-371)
+    def _rhs_c(self, q):
+        """euler.nonlinear_rhs set2c flux form (euler.py:474-487, 492-497)."""
+        U = np.moveaxis(q[1:4], 0, -1)
+        rho = self.rho0 + q[0]
+        Theta = self.Theta0 + q[4]
+        theta = Theta / rho
+        Pp = self.pprime_of(q)
+        out = np.empty_like(q)
+        out[0] = -self.div(U)
+        for m in range(3):
+            Fm = U[..., m][..., None] * U / rho[..., None]
+            Fm[..., m] += Pp
+            out[1 + m] = -self.div(Fm)
+        out[1:4] -= np.moveaxis(q[0][..., None] * self.gvec, -1, 0)
+        out[4] = -self.div(theta[..., None] * U)
+        out = self.dss_many(out)
+        out[1:4] = self.no_flux(out[1:4])
+        return out
+
+    # -- L_V(q): linear_operator(vertical_only=True) (euler.py:313-371)
     def linear(self, q):
+        if self.set_name == "set2c":
+            return self._linear_c(q)
         vel = np.moveaxis(q[1:4], 0, -1)
         P = self.G0 * q[0] + self.H0 * q[4]
         gradP = self.dvert(P)[..., None] * self.vert
@@ -361,7 +417,23 @@ class BoxOracle:
         out[1:4] = self.no_flux(np.moveaxis(mom, -1, 0))
         return out
 
-    # -- Schur pieces (imexcore.py:200-298), set2nc, dim='1d' ---------------
+    def _linear_c(self, q):
+        """set2c branch of linear_operator, vertical only (euler.py:350-361)."""
+        vel = np.moveaxis(q[1:4], 0, -1)
+        P = self.F0c * q[4]
+        gradP = self.dvert(P)[..., None] * self.vert
+        vv = np.einsum("...a,...a->...", vel, self.vert)
+        divU = self.dvert(vv)
+        adv = vv[..., None] * self.vert
+        out = np.zeros_like(q)
+        out[0] = -divU
+        mom = -(gradP + q[0][..., None] * self.gvec)
+        out[4] = -(self.theta0 * divU + np.einsum("...a,...a->...", adv, self.grad_theta0))
+        mom = np.einsum("...a,...a->...", mom, self.vert)[..., None] * self.vert
+        out[1:4] = self.no_flux(np.moveaxis(mom, -1, 0))
+        return out
+
+    # -- Schur pieces (imexcore.py:200-298), dim='1d' -------------------------
     def ainv(self, v, lam):
         """Sherman-Morrison inverse of I + lam^2 u w^T (imexcore.py:200-217)."""
         w = self.grad_theta0
@@ -378,22 +450,33 @@ class BoxOracle:
         return np.moveaxis(self.no_flux(np.moveaxis(vec, -1, 0)), 0, -1)
 
     def helm(self, vel, lam):
-        """imexcore._helmholtz_flux set2nc (imexcore.py:259-265)."""
+        """imexcore._helmholtz_flux (imexcore.py:259-268)."""
         vv = np.einsum("...a,...a->...", vel, self.vert)
+        if self.set_name == "set2c":
+            return self.F0c * lam * (self.theta0 * self.dvert(vv)
+                                     + np.einsum("...a,...a->...", self.grad_theta0, vel))
         return lam * (np.einsum("...a,...a->...", self.F0vec, vel)
                       + self.rho0 * self.G0 * self.dvert(vv))
 
     def up(self, P, lam):
         """imexcore._up set2nc (imexcore.py:245-257)."""
         gP = self.dvert(P)[..., None] * self.vert
-        v = self.ainv(lam * (gP / self.rho0[..., None]
-                             + (P / (self.G0 * self.rho0))[..., None] * self.gvec), lam)
+        if self.set_name == "set2c":
+            v = self.ainv(lam * (gP + (P / (self.F0c * self.theta0))[..., None] * self.gvec), lam)
+        else:
+            v = self.ainv(lam * (gP / self.rho0[..., None]
+                                 + (P / (self.G0 * self.rho0))[..., None] * self.gvec), lam)
         return self._nf(v)
 
     def schur_rhs(self, qe, lam):
         """imexcore.rhs_schur_build set2nc (imexcore.py:229-243)."""
-        Pe = self.G0 * qe[0] + self.H0 * qe[4]
         vel = np.moveaxis(qe[1:4], 0, -1)
+        if self.set_name == "set2c":
+            Pe = self.F0c * qe[4]
+            ua = self._nf(self.ainv(vel - (lam * (qe[0] - qe[4] / self.theta0))[..., None]
+                                    * self.gvec, lam))
+            return Pe - self.helm(ua, lam), ua
+        Pe = self.G0 * qe[0] + self.H0 * qe[4]
         coef = lam * self.H0 / (self.G0 * self.rho0)
         ua = self._nf(self.ainv(vel + (coef * qe[4])[..., None] * self.gvec, lam))
         return Pe - self.helm(ua, lam), ua
@@ -409,6 +492,12 @@ class BoxOracle:
         q[1:4] = np.moveaxis(vel, -1, 0)
         uv = np.einsum("...a,...a->...", vel, self.vert)
         adv = uv[..., None] * self.vert
+        if self.set_name == "set2c":   # imexcore.py:288-297
+            q[4] = P / self.F0c
+            q[0] = (P / (self.F0c * self.theta0)
+                    + lam / self.theta0 * np.einsum("...a,...a->...", adv, self.grad_theta0)
+                    - qe[4] / self.theta0 + qe[0])
+            return q
         q[4] = qe[4] - lam * np.einsum("...a,...a->...", adv, self.grad_theta0)
         q[0] = (P - self.H0 * q[4]) / self.G0
         return q
@@ -542,7 +631,12 @@ class BoxOracle:
         """cli.run_simulation dt rule (cli.py:187-194, euler.py:564-580)."""
         rho = self.rho0 + q[0]
         vel = np.moveaxis(q[1:4], 0, -1)
-        P = self.eos(rho, self.theta0 + q[4])
+        if self.set_name == "set2c":     # euler.py:572-574
+            vel = vel / rho[..., None]
+            theta = (self.Theta0 + q[4]) / rho
+        else:
+            theta = self.theta0 + q[4]
+        P = self.eos(rho, theta)
         cmax = float(np.max(np.linalg.norm(vel, axis=-1) + np.sqrt(GAMMA * P / rho)))
         _, dx_v = self.min_node_spacing()
         return courant * dx_v / cmax

@@ -38,8 +38,8 @@ _DP = ctypes.POINTER(ctypes.c_double)
 class RefDesc(ctypes.Structure):
     _fields_ = [(n, _DP) for n in (
         "rho0", "theta0", "P0f", "drho0", "dtheta0", "G0", "H0", "F0z", "rho0G0", "Pb",
-        "cx", "cy", "cz", "Dx", "Dy", "Dz")] + [
-        (n, ctypes.c_double) for n in ("g", "R", "P0", "gamma")]
+        "cx", "cy", "cz", "Dx", "Dy", "Dz", "Theta0", "F0c")] + [
+        (n, ctypes.c_double) for n in ("g", "R", "P0", "gamma")] + [("eqset", ctypes.c_int)]
 
 
 # exported symbol -> (restype, argtypes); this list IS the C ABI of hevi.h

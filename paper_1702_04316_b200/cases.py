@@ -39,15 +39,21 @@ def straka_lattice(mesh, ref, device="cuda"):
                           radii=(4000.0, 4000.0, 2000.0), device=device)
 
 
-def dt_for_courant(mesh, ref, q, courant):
+def dt_for_courant(mesh, ref, q, courant, set_name="set2nc"):
     """dt = C dx_v / max(|u| + c_s) (cli.py:187-194, euler.py:564-580)."""
     import torch
     c = ref.const
     rho0 = torch.as_tensor(ref.rho0, device=q.device)[:, None, None]
     theta0 = torch.as_tensor(ref.theta0, device=q.device)[:, None, None]
     rho = rho0 + q[0]
-    P = c.P0 * (rho * c.R * (theta0 + q[4]) / c.P0) ** c.gamma
-    speed = torch.sqrt(q[1] ** 2 + q[2] ** 2 + q[3] ** 2) + torch.sqrt(c.gamma * P / rho)
+    if set_name == "set2c":     # momentum and Theta' (euler.py:572-574)
+        vel = q[1:4] / rho
+        theta = (torch.as_tensor(ref.Theta0, device=q.device)[:, None, None] + q[4]) / rho
+    else:
+        vel = q[1:4]
+        theta = theta0 + q[4]
+    P = c.P0 * (rho * c.R * theta / c.P0) ** c.gamma
+    speed = torch.sqrt(vel[0] ** 2 + vel[1] ** 2 + vel[2] ** 2) + torch.sqrt(c.gamma * P / rho)
     cmax = float(speed.max())
     _, dx_v = mesh.min_node_spacing()
     return courant * dx_v / cmax

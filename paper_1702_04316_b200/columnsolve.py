@@ -89,7 +89,7 @@ def build_column_jacobian(problem) -> ColumnJacobian:
         raise ValueError("column Jacobians require the 1D implicit form")
     if problem.form != "schur":
         raise NotImplementedError("the device path implements the Schur (pressure) form")
-    plan = problem.disc.plan_for(problem.ref)
+    plan = problem.disc.plan_for(problem.ref, problem.set_name)
     lam = float(problem.lam)
     space = unique_space(problem.disc.mesh)
     if lam == 0.0:
@@ -182,5 +182,5 @@ def get_factors(problem) -> ColumnJacobian:
 def solve_direct(problem, q_e):
     """One direct implicit solve (columnsolve.py:191-210): the fused device
     column kernel with the shared per-lam factor."""
-    plan = problem.disc.plan_for(problem.ref)
+    plan = problem.disc.plan_for(problem.ref, problem.set_name)
     return plan.apply_evec("solve", q_e, lam=float(problem.lam))

@@ -75,6 +75,7 @@ struct Geo {
 struct Lev {
     const double *rho0, *theta0, *P0f, *drho0, *dth0, *G0, *H0, *F0z, *rho0G0;
     const double *E0, *c0, *irt0;   // EOS(rho0, theta0), E0 - P0f, 1/(rho0 theta0)
+    const double *Th0, *iTh0, *F0c; // set2c: Theta0 = rho0 theta0, 1/Theta0, gamma P0f / Theta0
 };
 
 struct Phys {
@@ -592,9 +593,9 @@ struct FArgs {
     double g, lam;
     const double* cz;
     const double* Dz;
-    int N, nez, M, ainv_identity;
+    int N, nez, M, ainv_identity, eqset;
     double* lamtab;  // coefS | uA | den
-    double* vtab;    // 12 x M tables of the v2 column kernel
+    double* vtab;    // V_NT x M tables of the v2 column kernel
     double* A;       // M*M dense, row-major, zeroed
     unsigned* flags;
 };
@@ -625,6 +626,11 @@ __global__ void k_lamtab(const FArgs a) {
     t[9 * M + k] = 1.0 / a.lv.rho0[k];
     t[10 * M + k] = 1.0 / (a.lv.G0[k] * a.lv.rho0[k]);
     t[11 * M + k] = 1.0 / a.lv.G0[k];
+    // set2c (imexcore.py:239-240, 254-255, 266-268, 288-297): G0 = theta0
+    t[12 * M + k] = a.lv.F0c[k];
+    t[13 * M + k] = a.lv.theta0[k];
+    t[14 * M + k] = 1.0 / (a.lv.F0c[k] * a.lv.theta0[k]);
+    t[15 * M + k] = 1.0 / a.lv.theta0[k];
 }
 
 __device__ double f_unit(int l, int j) { return l == j ? 1.0 : 0.0; }
@@ -651,7 +657,10 @@ __global__ void k_probe(const FArgs a) {
                 acc += acc2;
             }
             const double dP = a.cz[k] * acc;
-            double v = lam * (dP / a.lv.rho0[k] + (f_unit(k, j) / (a.lv.G0[k] * a.lv.rho0[k])) * gr);
+            // imexcore._up (imexcore.py:250-255)
+            double v = a.eqset == 0
+                           ? lam * (dP / a.lv.rho0[k] + (f_unit(k, j) / (a.lv.G0[k] * a.lv.rho0[k])) * gr)
+                           : lam * (dP + (f_unit(k, j) / (a.lv.F0c[k] * a.lv.theta0[k])) * gr);
             if (!a.ainv_identity) {
                 const double uA = a.lamtab[M + k], den = a.lamtab[2 * M + k];
                 v = v - uA * ((a.lv.dth0[k] * v) / den);
@@ -674,8 +683,10 @@ __global__ void k_probe(const FArgs a) {
                 acc += acc2;
             }
             const double dup = a.cz[k] * acc;
-            // imexcore.py:264-265, 270-271
-            const double helm = lam * (a.lv.F0z[k] * upv(k) + a.lv.rho0G0[k] * dup);
+            // imexcore._helmholtz_flux (imexcore.py:263-268), lhs_schur (:270-271)
+            const double helm =
+                a.eqset == 0 ? lam * (a.lv.F0z[k] * upv(k) + a.lv.rho0G0[k] * dup)
+                             : a.lv.F0c[k] * lam * (a.lv.theta0[k] * dup + a.lv.dth0[k] * upv(k));
             a.A[(long long)k * M + j] = f_unit(k, j) - helm;
         }
     }
@@ -895,6 +906,7 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 
 #include "explicit_v2.cuh"
 #include "explicit_v3.cuh"
+#include "explicit_c.cuh"
 #include "solve_v2.cuh"
 
 }  // namespace
@@ -926,6 +938,7 @@ struct hevi_plan {
     unsigned* h_flags = nullptr;
     std::map<long long, Factor> factors;
     double bc[16];
+    int eqset = 0;   // 0: set2nc, 1: set2c
     unsigned long long* d_dbg = nullptr;
     bool use_v2 = true;
     bool use_v3 = false;
@@ -1162,7 +1175,84 @@ int run_e2(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st, bool&
     return fail("bad mode");
 }
 
+// ---- set2c explicit dispatch ---------------------------------------------
+template <int N, int NY>
+struct TileC {
+    static constexpr int TX = 0, TY = 0;
+};
+template <> struct TileC<1, 1> { static constexpr int TX = 8, TY = 8; };
+template <> struct TileC<2, 2> { static constexpr int TX = 4, TY = 4; };
+template <> struct TileC<3, 3> { static constexpr int TX = 3, TY = 3; };
+template <> struct TileC<4, 4> { static constexpr int TX = 2, TY = 2; };
+template <> struct TileC<5, 5> { static constexpr int TX = 1, TY = 1; };
+template <> struct TileC<6, 6> { static constexpr int TX = 1, TY = 1; };
+template <> struct TileC<2, 1> { static constexpr int TX = 16, TY = 1; };
+template <> struct TileC<3, 1> { static constexpr int TX = 12, TY = 1; };
+template <> struct TileC<4, 1> { static constexpr int TX = 8, TY = 1; };
+template <> struct TileC<5, 1> { static constexpr int TX = 6, TY = 1; };
+template <> struct TileC<6, 1> { static constexpr int TX = 5, TY = 1; };
+template <> struct TileC<7, 1> { static constexpr int TX = 4, TY = 1; };
+template <> struct TileC<8, 1> { static constexpr int TX = 4, TY = 1; };
+
+template <int N, int NY, int MODE>
+int launch_c(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
+    constexpr int TX = TileC<N, NY>::TX, TY = TileC<N, NY>::TY;
+    if constexpr (TX == 0) {
+        return fail("set2c: unsupported polynomial order for the device path");
+    } else {
+        using T = ECT<N, NY, TX, TY>;
+        auto kern = k_explicit_c<N, NY, TX, TY, MODE>;
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
+            attr = true;
+        }
+        const Geo& g = pl->g;
+        dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
+        kern<<<grid, T::BLK, T::SMEM, st>>>(a);
+        CK(cudaGetLastError());
+        return HEVI_OK;
+    }
+}
+
+template <int MODE>
+int dispatch_c(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
+    const int N = pl->N, Ny = pl->Ny;
+    if (Ny == N) {
+        switch (N) {
+            case 1: return launch_c<1, 1, MODE>(pl, a, st);
+            case 2: return launch_c<2, 2, MODE>(pl, a, st);
+            case 3: return launch_c<3, 3, MODE>(pl, a, st);
+            case 4: return launch_c<4, 4, MODE>(pl, a, st);
+            case 5: return launch_c<5, 5, MODE>(pl, a, st);
+            case 6: return launch_c<6, 6, MODE>(pl, a, st);
+        }
+    } else if (Ny == 1) {
+        switch (N) {
+            case 2: return launch_c<2, 1, MODE>(pl, a, st);
+            case 3: return launch_c<3, 1, MODE>(pl, a, st);
+            case 4: return launch_c<4, 1, MODE>(pl, a, st);
+            case 5: return launch_c<5, 1, MODE>(pl, a, st);
+            case 6: return launch_c<6, 1, MODE>(pl, a, st);
+            case 7: return launch_c<7, 1, MODE>(pl, a, st);
+            case 8: return launch_c<8, 1, MODE>(pl, a, st);
+        }
+    }
+    return fail("set2c: unsupported polynomial order for the device path");
+}
+
 int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
+    if (pl->eqset == 1) {
+        switch (mode) {
+            case M_R: return dispatch_c<M_R>(pl, a, st);
+            case M_L: return dispatch_c<M_L>(pl, a, st);
+            case M_S1: return dispatch_c<M_S1>(pl, a, st);
+            case M_S2: return dispatch_c<M_S2>(pl, a, st);
+            case M_S3: return dispatch_c<M_S3>(pl, a, st);
+            case M_RK: return dispatch_c<M_RK>(pl, a, st);
+        }
+        return fail("bad mode");
+    }
     if (pl->use_v2 && (pl->g.px % 2) == 0) {
         bool done = false;
         int rc = run_e2(pl, mode, a, st, done);
@@ -1253,14 +1343,25 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
     if (smem > 225 * 1024) return fail("column too tall for the v2 column kernel");
     static size_t attr = 0;
     if (attr < smem) {
-        CK(cudaFuncSetAttribute(k_solve2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_solve2<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
         attr = smem;
     }
     const int NYo = g.slab ? 1 : pl->N;
     const long long cntx = (long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0);
     const long long cnty = (long long)(g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
     const int blocks = (int)((cntx * cnty + T - 1) / T);
-    k_solve2<N><<<blocks, T, smem, st>>>(a);
+    if (pl->eqset == 1) {
+        static size_t attrc = 0;
+        if (attrc < smem) {
+            CK(cudaFuncSetAttribute(k_solve2<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+            attrc = smem;
+        }
+        k_solve2<N, true><<<blocks, T, smem, st>>>(a);
+    } else {
+        k_solve2<N, false><<<blocks, T, smem, st>>>(a);
+    }
     CK(cudaGetLastError());
     return HEVI_OK;
 }
@@ -1289,6 +1390,14 @@ int run_s2(const hevi_plan* pl, const Factor* f, const SArgs& a, cudaStream_t st
 
 int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st) {
     {
+        if (pl->eqset == 1) {
+            const Factor* f = find_factor(pl, a.lam);
+            bool done = false;
+            int rc = f ? run_s2(pl, f, a, st, done) : fail("lam not factored");
+            if (rc) return rc;
+            if (!done) return fail("set2c: column too tall for the device column kernel");
+            return HEVI_OK;
+        }
         const Factor* f = find_factor(pl, a.lam);
         bool done = false;
         if (f) {
@@ -1403,6 +1512,15 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     h.insert(h.end(), rd->Pb, rd->Pb + Z);
     for (int k = 0; k < Z; ++k) h.push_back(rd->Pb[k] - rd->P0f[k]);
     for (int k = 0; k < Z; ++k) h.push_back(1.0 / (rd->rho0[k] * rd->theta0[k]));
+    // set2c: Theta0, 1/Theta0, F0 (euler.py:103-113)
+    h.insert(h.end(), rd->Theta0, rd->Theta0 + Z);
+    for (int k = 0; k < Z; ++k) h.push_back(1.0 / rd->Theta0[k]);
+    h.insert(h.end(), rd->F0c, rd->F0c + Z);
+    pl->eqset = rd->eqset;
+    if (rd->eqset != 0 && rd->eqset != 1) {
+        delete pl;
+        return fail("eqset must be 0 (set2nc) or 1 (set2c)");
+    }
     pl->ainv_identity = 1;
     for (int k = 0; k < Z; ++k)
         if (rd->dtheta0[k] != 0.0) pl->ainv_identity = 0;
@@ -1428,7 +1546,8 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     pl->Dz = pl->Dy + ndy;
     const double* eos = pl->Dz + nd;
     pl->lv = {d,         d + Z,     d + 2 * Z, d + 3 * Z, d + 4 * Z, d + 5 * Z,
-              d + 6 * Z, d + 7 * Z, d + 8 * Z, eos,       eos + Z,   eos + 2 * Z};
+              d + 6 * Z, d + 7 * Z, d + 8 * Z, eos,       eos + Z,   eos + 2 * Z,
+              eos + 3 * Z, eos + 4 * Z, eos + 5 * Z};
     // binomial coefficients C(gamma, k) of the P' series
     {
         double cb = 1.0;
@@ -1480,7 +1599,7 @@ int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
         CK(cudaMalloc(&f.LU, sizeof(double) * M * M));
         CK(cudaMalloc(&f.LUb, sizeof(double) * M * (2 * M - 1)));
         CK(cudaMalloc(&f.lamtab, sizeof(double) * 3 * M));
-        CK(cudaMalloc(&f.vtab, sizeof(double) * 12 * M));
+        CK(cudaMalloc(&f.vtab, sizeof(double) * V_NT * M));
         CK(cudaMalloc(&f.LU2, sizeof(double) * M * (4 * pl->N + 1)));
         CK(cudaMalloc(&f.rU, sizeof(double) * M));
         CK(cudaMalloc(&f.d_nb, sizeof(int)));
@@ -1495,6 +1614,7 @@ int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
         a.nez = pl->g.nez;
         a.M = M;
         a.ainv_identity = pl->ainv_identity;
+        a.eqset = pl->eqset;
         a.lamtab = f.lamtab;
         a.vtab = f.vtab;
         a.A = f.A;

@@ -29,9 +29,10 @@ struct S2Args {
     const double* src_uv;  // optional: copy u,v (with no-flux zeroing)
 };
 
-enum { V_G0 = 0, V_H0, V_F0Z, V_RG, V_CZ, V_COEF, V_UA, V_DEN, V_DTH0, V_IRHO0, V_IG0R, V_IG0, V_NT };
+enum { V_G0 = 0, V_H0, V_F0Z, V_RG, V_CZ, V_COEF, V_UA, V_DEN, V_DTH0, V_IRHO0, V_IG0R, V_IG0,
+       V_F0C, V_TH0, V_IFT, V_ITH0, V_NT };
 
-template <int N>
+template <int N, bool SC>   // SC: conservative set set2c
 __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     constexpr int W = 4 * N + 1;
     extern __shared__ __align__(16) double sm2[];
@@ -70,8 +71,9 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     const long long ls = (long long)g.lY * g.px;    // level stride
 #define TB(t, k) tb[(t) * M + (k)]
 
-    auto ua_of = [&](double we, double te, int k) -> double {
-        double v = we + (TB(V_COEF, k) * te) * gr;
+    // ua_z of the Schur RHS (imexcore.py:236-240); `re` only enters set2c
+    auto ua_of2 = [&](double re, double we, double te, int k) -> double {
+        double v = SC ? we - (lam * (re - te * TB(V_ITH0, k))) * gr : we + (TB(V_COEF, k) * te) * gr;
         if (!ident) v = v - TB(V_UA, k) * ((TB(V_DTH0, k) * v) / TB(V_DEN, k));
         return (k == 0 || k == M - 1) ? 0.0 : v;
     };
@@ -82,8 +84,8 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     for (int i = 0; i < 3 * N; ++i) yw[i] = 0.0;
     {
         const double re = Ps[0], we = Ps[3 * fs], te = Ps[4 * fs];
-        uaw[0] = ua_of(we, te, 0);
-        Pew[0] = TB(V_G0, 0) * re + TB(V_H0, 0) * te;
+        uaw[0] = ua_of2(re, we, te, 0);
+        Pew[0] = SC ? TB(V_F0C, 0) * te : TB(V_G0, 0) * re + TB(V_H0, 0) * te;
     }
     double carry = 0.0;
     for (int e = 0; e < nez; ++e) {
@@ -99,8 +101,8 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
 #pragma unroll
         for (int l = 1; l <= N; ++l) {
             const int k = k0 + l;
-            uaw[l] = ua_of(we[l - 1], te[l - 1], k);
-            Pew[l] = TB(V_G0, k) * re[l - 1] + TB(V_H0, k) * te[l - 1];
+            uaw[l] = ua_of2(re[l - 1], we[l - 1], te[l - 1], k);
+            Pew[l] = SC ? TB(V_F0C, k) * te[l - 1] : TB(V_G0, k) * re[l - 1] + TB(V_H0, k) * te[l - 1];
         }
 #pragma unroll
         for (int l = 0; l < N; ++l) {
@@ -110,7 +112,9 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
             for (int m = 0; m <= N; ++m) d = fma(sD[l * (N + 1) + m], uaw[m], d);
             if (l == 0 && e > 0) d += carry;
             const double dua = TB(V_CZ, k) * d;
-            const double rhs = Pew[l] - lam * (TB(V_F0Z, k) * uaw[l] + TB(V_RG, k) * dua);
+            // imexcore._helmholtz_flux (imexcore.py:263-268)
+            const double rhs = SC ? Pew[l] - TB(V_F0C, k) * lam * (TB(V_TH0, k) * dua + TB(V_DTH0, k) * uaw[l])
+                                  : Pew[l] - lam * (TB(V_F0Z, k) * uaw[l] + TB(V_RG, k) * dua);
             double s = 0.0;
             const double* Lr = LU + k * W;
 #pragma unroll
@@ -134,7 +138,8 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     {   // top level: row N of the last element, boundary
         const int k = M - 1;
         const double dua = TB(V_CZ, k) * carry;
-        const double rhs = Pew[N] - lam * (TB(V_F0Z, k) * uaw[N] + TB(V_RG, k) * dua);
+        const double rhs = SC ? Pew[N] - TB(V_F0C, k) * lam * (TB(V_TH0, k) * dua + TB(V_DTH0, k) * uaw[N])
+                              : Pew[N] - lam * (TB(V_F0Z, k) * uaw[N] + TB(V_RG, k) * dua);
         double s = 0.0;
         const double* Lr = LU + k * W;
 #pragma unroll
@@ -149,11 +154,13 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     for (int i = 0; i <= 3 * N; ++i) xw[i] = 0.0;
     xw[N] = Y[(M - 1) * T + tid] * rU[M - 1];
 
-    auto extract = [&](int k, double Pk, double dsum, double we, double te) {
+    auto extract = [&](int k, double Pk, double dsum, double re, double we, double te) {
         const bool bz = (k == 0) || (k == M - 1);
         const double dP = TB(V_CZ, k) * dsum;
-        double up = lam * (dP * TB(V_IRHO0, k) + (Pk * TB(V_IG0R, k)) * gr);
-        double ua = we + (TB(V_COEF, k) * te) * gr;
+        // imexcore._up (imexcore.py:245-257)
+        double up = SC ? lam * (dP + (Pk * TB(V_IFT, k)) * gr)
+                       : lam * (dP * TB(V_IRHO0, k) + (Pk * TB(V_IG0R, k)) * gr);
+        double ua = SC ? we - (lam * (re - te * TB(V_ITH0, k))) * gr : we + (TB(V_COEF, k) * te) * gr;
         if (!ident) {
             ua = ua - TB(V_UA, k) * ((TB(V_DTH0, k) * ua) / TB(V_DEN, k));
             up = up - TB(V_UA, k) * ((TB(V_DTH0, k) * up) / TB(V_DEN, k));
@@ -163,8 +170,14 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
             up = 0.0;
         }
         const double w = ua - up;
-        const double th = te - lam * (w * TB(V_DTH0, k));
-        const double rho = (Pk - TB(V_H0, k) * th) * TB(V_IG0, k);
+        double th, rho;
+        if (SC) {   // imexcore.py:288-297
+            th = Pk / TB(V_F0C, k);
+            rho = ((Pk * TB(V_IFT, k) + (lam * TB(V_ITH0, k)) * (w * TB(V_DTH0, k))) - te * TB(V_ITH0, k)) + re;
+        } else {    // imexcore.py:280-287
+            th = te - lam * (w * TB(V_DTH0, k));
+            rho = (Pk - TB(V_H0, k) * th) * TB(V_IG0, k);
+        }
         const long long o = (long long)k * ls;
         Oo[o] = rho;
         Oo[o + 3 * fs] = w;
@@ -180,12 +193,13 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
 
     for (int e = nez - 1; e >= 0; --e) {
         const int k0 = e * N;
-        double we[N], te[N];
+        double we[N], te[N], ro[N];
 #pragma unroll
         for (int l = 1; l <= N; ++l) {
             const long long o = (long long)(k0 + l) * ls;
             we[l - 1] = Po[o + 3 * fs];
             te[l - 1] = Po[o + 4 * fs];
+            ro[l - 1] = SC ? Po[o] : 0.0;
         }
 #pragma unroll
         for (int l = N - 1; l >= 0; --l) {
@@ -209,7 +223,7 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
                 for (int m = 0; m <= N; ++m) d2 = fma(sD[m], xw[N + m], d2);
                 d += d2;
             }
-            extract(k, xw[l], d, we[l - 1], te[l - 1]);
+            extract(k, xw[l], d, ro[l - 1], we[l - 1], te[l - 1]);
         }
         if (e > 0) {
 #pragma unroll
@@ -220,7 +234,7 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
         double d = 0.0;
 #pragma unroll
         for (int m = 0; m <= N; ++m) d = fma(sD[m], xw[m], d);
-        extract(0, xw[0], d, Po[3 * fs], Po[4 * fs]);
+        extract(0, xw[0], d, SC ? Po[0] : 0.0, Po[3 * fs], Po[4 * fs]);
     }
 #undef TB
 }

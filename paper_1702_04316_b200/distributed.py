@@ -132,9 +132,10 @@ class HaloExchange:
 class DistributedStepper:
     """One rank of the partitioned fused ARK2 step."""
 
-    def __init__(self, mesh, ref, disc, dt, px, py, rank, exchange=None, tableau=None):
+    def __init__(self, mesh, ref, disc, dt, px, py, rank, exchange=None, tableau=None,
+                 set_name="set2nc"):
         self.block = make_block(mesh, px, py, rank)
-        self.plan = HeviPlan(mesh, ref, disc, window=self.block.window)
+        self.plan = HeviPlan(mesh, ref, disc, window=self.block.window, set_name=set_name)
         self.exchange = exchange if exchange is not None else HaloExchange(mesh, px, py, rank)
         self.tableau = tableau or imexcore.ark2_tableau()
         self.tab = tableau_array(self.tableau)

@@ -6,9 +6,9 @@ Same entry points and argument meaning as the reference
 ``nonlinear_rhs``, ``vertical_restriction``, ``linear_operator``
 (``vertical_only=True``), ``linearized_pressure``, ``equation_of_state``.
 Arrays in and out are E-vectors ``(5, nel, nqt, nqs, nqr)`` (numpy or torch);
-the arithmetic runs in libhevi.so on the GPU.  Supported: cG, ``set2nc``.
-Everything else the reference accepts (``set2c``, dG, the full 3D linear
-operator) is outside the north-star path and raises ``NotImplementedError``.
+the arithmetic runs in libhevi.so on the GPU.  Supported: cG, ``set2nc``
+(primary) and ``set2c`` (conservative flux form).  dG and the full 3D linear
+operator are outside the north-star path and raise ``NotImplementedError``.
 """
 from __future__ import annotations
 
@@ -71,6 +71,23 @@ class ReferenceState:
             self._cache["F0z"] = self.G0_nc * self.drho0 + self.H0_nc * self.dtheta0
         return self._cache["F0z"]
 
+    # --- set2c coefficients (euler.py:102-122) ---
+    @property
+    def Theta0(self):
+        if "Theta0" not in self._cache:
+            self._cache["Theta0"] = self.rho0 * self.theta0
+        return self._cache["Theta0"]
+
+    @property
+    def F0_c(self):
+        if "F0_c" not in self._cache:
+            self._cache["F0_c"] = self.const.gamma * self.P0f / self.Theta0
+        return self._cache["F0_c"]
+
+    @property
+    def G0_c(self):
+        return self.theta0
+
     @property
     def rho0G0(self):
         """rho0 * G0, the factor of the vertical divergence (imexcore.py:265)."""
@@ -119,6 +136,29 @@ def isothermal_reference(mesh: sg.BoxMesh, T_bg: float,
                           P0f=P0f, drho0=drho0, dtheta0=dth0)
 
 
+def linearized_pressure(q, ref: ReferenceState, set_name: str, mesh: sg.BoxMesh = None):
+    """Perturbation pressure of the linearised EOS (euler.py:188-194): G0 rho' +
+    H0 theta' (set2nc) or F0 Theta' (set2c).  ``q`` is an E-vector (numpy or
+    torch) of ``mesh`` (host/diagnostic helper; the kernels form it inline)."""
+    if set_name not in ("set2nc", "set2c"):
+        raise ValueError(f"unknown equation set {set_name!r}")
+    if mesh is None:
+        raise ValueError("linearized_pressure needs the mesh to map nodes to levels")
+    nel, nt, ns, nr = mesh.nshape
+    kz = np.arange(nel) // (mesh.nx * mesh.ny)
+    lev = (kz[:, None] * mesh.N + np.arange(nt)[None, :])[:, :, None, None]
+
+    def per_node(a):
+        t = np.broadcast_to(a[lev], (nel, nt, ns, nr))
+        if isinstance(q, np.ndarray):
+            return t
+        import torch
+        return torch.as_tensor(np.ascontiguousarray(t), device=q.device)
+    if set_name == "set2nc":
+        return per_node(ref.G0_nc) * q[0] + per_node(ref.H0_nc) * q[4]
+    return per_node(ref.F0_c) * q[4]
+
+
 def equation_of_state(rho, theta, const: GasConstants):
     """Full nonlinear pressure P = P0 (rho R theta / P0)^gamma (euler.py:180-185).
     Host helper for diagnostics; the step evaluates it inside the kernels."""
@@ -138,12 +178,12 @@ class Discretization:
     cz: np.ndarray
     _plans: dict = field(default_factory=dict)
 
-    def plan_for(self, ref: ReferenceState):
+    def plan_for(self, ref: ReferenceState, set_name: str = "set2nc"):
         from .plan import HeviPlan
-        key = id(ref)
+        key = (id(ref), set_name)
         ent = self._plans.get(key)
         if ent is None or ent[0] is not ref:
-            ent = (ref, HeviPlan(self.mesh, ref, self))
+            ent = (ref, HeviPlan(self.mesh, ref, self, set_name=set_name))
             self._plans[key] = ent
         return ent[1]
 
@@ -162,15 +202,14 @@ def _check_set(set_name: str, dg: bool = False):
         raise ValueError(f"unknown equation set {set_name!r}")
     if dg:
         raise NotImplementedError("dG is outside the HEVI direct path (SURVEY 2.4)")
-    if set_name != "set2nc":
-        raise NotImplementedError("the B200 HEVI path implements the set2nc equation set")
 
 
 def nonlinear_rhs(q, ref: ReferenceState, disc: Discretization, set_name: str,
                   dg: bool = False):
-    """R(q), cG set2nc with DSS and no-flux projection (euler.py:438-497)."""
+    """R(q), cG set2nc (advective) or set2c (flux form), with DSS and no-flux
+    projection (euler.py:438-497)."""
     _check_set(set_name, dg)
-    return disc.plan_for(ref).apply_evec("rhs", q)
+    return disc.plan_for(ref, set_name).apply_evec("rhs", q)
 
 
 def linear_operator(q, ref: ReferenceState, disc: Discretization, set_name: str,
@@ -180,7 +219,7 @@ def linear_operator(q, ref: ReferenceState, disc: Discretization, set_name: str,
     if not vertical_only:
         raise NotImplementedError("the full 3D linear operator belongs to 3D-IMEX "
                                   "(SURVEY 8(f) 'next')")
-    return disc.plan_for(ref).apply_evec("linear", q)
+    return disc.plan_for(ref, set_name).apply_evec("linear", q)
 
 
 def vertical_restriction(q, ref: ReferenceState, disc: Discretization, set_name: str):

@@ -87,7 +87,7 @@ def rk35_step(q, dt: float, rhs):
     ``euler.RHS`` the five stages run as fused device launches."""
     if isinstance(rhs, euler.RHS):
         from .plan import to_device
-        plan = rhs.disc.plan_for(rhs.ref)
+        plan = rhs.disc.plan_for(rhs.ref, rhs.set_name)
         E, back = to_device(q)
         Q = plan.e2l(E)
         work = plan.workspace()
@@ -209,7 +209,7 @@ def ark_imex_step(q, dt: float, tableau: ButcherPair, problem, rhs):
     """One additive Runge-Kutta IMEX step (imexcore.py:385-414)."""
     if _is_fused(problem, rhs) and tableau.stages == 3:
         from .plan import tableau_array, to_device
-        plan = problem.disc.plan_for(problem.ref)
+        plan = problem.disc.plan_for(problem.ref, problem.set_name)
         problem.lam = tableau.diag * dt
         E, back = to_device(q)
         Q = plan.e2l(E)

@@ -36,7 +36,7 @@ def raise_for_flags(flags: int):
 
 
 class HeviPlan:
-    def __init__(self, mesh, ref, disc, window=None):
+    def __init__(self, mesh, ref, disc, window=None, set_name="set2nc"):
         import torch
         nv.require_cuda()
         self.lib = nv.load()
@@ -59,8 +59,12 @@ class HeviPlan:
         self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (
             ref.rho0, ref.theta0, ref.P0f, ref.drho0, ref.dtheta0, ref.G0_nc, ref.H0_nc,
             ref.F0z_nc, ref.rho0G0, Pb, disc.cx, disc.cy, disc.cz,
-            mesh.quad_r.D, mesh.quad_s.D, mesh.quad_t.D)]
-        rd = nv.RefDesc(*[_dp(a) for a in self._keep], c.g, c.R, c.P0, c.gamma)
+            mesh.quad_r.D, mesh.quad_s.D, mesh.quad_t.D, ref.Theta0, ref.F0_c)]
+        if set_name not in ("set2nc", "set2c"):
+            raise ValueError(f"unknown equation set {set_name!r}")
+        self.set_name = set_name
+        rd = nv.RefDesc(*[_dp(a) for a in self._keep], c.g, c.R, c.P0, c.gamma,
+                        1 if set_name == "set2c" else 0)
         h = ctypes.c_void_p()
         nv.check(self.lib.hevi_plan_create(ctypes.byref(h), ctypes.byref(gd), ctypes.byref(rd)))
         self.h = h

@@ -8,8 +8,8 @@ from .plan import tableau_array
 
 
 class HeviStepper:
-    def __init__(self, disc, ref, dt, tableau=None, check_every=1):
-        self.plan = disc.plan_for(ref)
+    def __init__(self, disc, ref, dt, tableau=None, check_every=1, set_name="set2nc"):
+        self.plan = disc.plan_for(ref, set_name)
         self.tableau = tableau or imexcore.ark2_tableau()
         self.tab = tableau_array(self.tableau)
         self.dt = float(dt)

@@ -25,7 +25,16 @@ CASES = {
                          background="isothermal", courant=15.0),
     "straka_n7": dict(nx=32, ny=1, nz=4, Lx=51_200.0, Ly=None, Lz=6_400.0, N=7,
                       slab=True, courant=0.7),
+    # conservative equation set (set2c, flux form)
+    "slab_aniso_c": dict(nx=5, ny=1, nz=4, Lx=20_000.0, Ly=None, Lz=1000.0, N=4,
+                         slab=True, courant=15.0, set_name="set2c"),
+    "box3d_n4_c": dict(nx=4, ny=4, nz=4, Lx=16_000.0, Ly=16_000.0, Lz=400.0, N=4,
+                       courant=15.0, set_name="set2c"),
 }
+
+
+def set_of(name):
+    return CASES[name].get("set_name", "set2nc")
 
 
 def pytest_configure(config):
@@ -36,11 +45,11 @@ def load_golden(name):
     return np.load(os.path.join(GOLDEN, f"{name}.npz"))
 
 
-def oracle_for(name):
+def oracle_for(name, pprime="reference"):
     from oracle.hevi_oracle import BoxOracle
     kw = dict(CASES[name])
     kw.pop("courant")
-    return BoxOracle(**kw)
+    return BoxOracle(**kw, pprime=pprime)   # set_name passes through
 
 
 def rel_scalar(a, b):

@@ -131,7 +131,7 @@ def continuous_random_state(disc, ref, seed, amp=1e-3, slab=True):
     return amp * scale[:, None, None, None, None] * q
 
 
-def bubble_state(mesh, ref, disc, theta_c, centre, radii, slab):
+def bubble_state(mesh, ref, disc, theta_c, centre, radii, slab, set_name="set2nc"):
     c = mesh.coords
     if slab:
         r = np.sqrt(((c[..., 0] - centre[0]) / radii[0]) ** 2
@@ -143,19 +143,19 @@ def bubble_state(mesh, ref, disc, theta_c, centre, radii, slab):
     th = np.where(r <= 1.0, 0.5 * theta_c * (1.0 + np.cos(np.pi * r)), 0.0)
     q = np.zeros((5,) + mesh.nshape)
     q[0] = ref.rho0 * (ref.theta0 / (ref.theta0 + th) - 1.0)
-    q[4] = th
+    q[4] = 0.0 if set_name == "set2c" else th     # bench.py:118-123
     return sg.apply_dss_many(q, disc.dss)
 
 
-def dt_for(mesh, ref, disc, q, C):
+def dt_for(mesh, ref, disc, q, C, set_name="set2nc"):
     """cli.run_simulation dt rule (cli.py:187-194)."""
     dx_h, dx_v = euler.min_node_spacing(mesh)
-    ch0, cv0 = euler.courant_numbers(q, ref, disc, 1.0, "set2nc")
+    ch0, cv0 = euler.courant_numbers(q, ref, disc, 1.0, set_name)
     return C * dx_v / (cv0 * dx_v)
 
 
 def run_case(name, mesh, N_s, slab, ops_seed, lam, bubble, C, nsteps, keep,
-             background="hydrostatic"):
+             background="hydrostatic", set_name="set2nc"):
     if background == "hydrostatic":
         ref = euler.hydrostatic_reference(mesh, 300.0)
     else:
@@ -167,9 +167,9 @@ def run_case(name, mesh, N_s, slab, ops_seed, lam, bubble, C, nsteps, keep,
     # operator level on a continuous random state
     qr = continuous_random_state(disc, ref, ops_seed, slab=slab)
     out["ops_q"] = L(qr)
-    out["ops_R"] = L(euler.nonlinear_rhs(qr, ref, disc, "set2nc"))
-    out["ops_L"] = L(euler.vertical_restriction(qr, ref, disc, "set2nc"))
-    prob = imx.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="schur",
+    out["ops_R"] = L(euler.nonlinear_rhs(qr, ref, disc, set_name))
+    out["ops_L"] = L(euler.vertical_restriction(qr, ref, disc, set_name))
+    prob = imx.ImplicitProblem(disc=disc, ref=ref, set_name=set_name, form="schur",
                                dim="1d", solver=imx.SolverSpec(method="direct"))
     prob.lam = lam
     out["ops_lam"] = np.array(lam)
@@ -183,13 +183,13 @@ def run_case(name, mesh, N_s, slab, ops_seed, lam, bubble, C, nsteps, keep,
     out["col_nb"] = np.array(cj.bandwidth)
     out["col_spread"] = np.array(np.abs(A - A[0:1]).max())
     # ARK2 HEVI steps from the bubble IC
-    q = bubble_state(mesh, ref, disc, *bubble, slab=slab)
-    dt = dt_for(mesh, ref, disc, q, C)
+    q = bubble_state(mesh, ref, disc, *bubble, slab=slab, set_name=set_name)
+    dt = dt_for(mesh, ref, disc, q, C, set_name)
     out["step_q0"] = L(q)
     out["step_dt"] = np.array(dt)
-    prob = imx.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="schur",
+    prob = imx.ImplicitProblem(disc=disc, ref=ref, set_name=set_name, form="schur",
                                dim="1d", solver=imx.SolverSpec(method="direct"))
-    rhs = lambda s: euler.nonlinear_rhs(s, ref, disc, "set2nc")  # noqa: E731
+    rhs = lambda s: euler.nonlinear_rhs(s, ref, disc, set_name)  # noqa: E731
     tab = imx.ark2_tableau()
     for k in range(1, nsteps + 1):
         q = imx.ark_imex_step(q, dt, tab, prob, rhs)
@@ -259,6 +259,16 @@ def main():
     run_rk35_case("rk35_box3d_n4", mesh, 4, False,
                   bubble=(0.5, (8_000.0, 8_000.0, 200.0), (4000.0, 4000.0, 100.0)),
                   C=1.0, nsteps=10, keep=(1, 10))
+    # 6. conservative set (set2c, flux form) on the slab and the 3D box
+    mesh = sg.build_box_mesh(5, 4, 20_000.0, 1000.0, 4)
+    mesh.meta["ny"] = 1
+    run_case("slab_aniso_c", mesh, 1, True, ops_seed=33, lam=0.8,
+             bubble=(0.5, (10_000.0, 0.0, 350.0), (2000.0, 1.0, 250.0)),
+             C=15.0, nsteps=10, keep=(1, 10), set_name="set2c")
+    mesh = box3d_mesh(4, 4, 4, 16_000.0, 16_000.0, 400.0, 4)
+    run_case("box3d_n4_c", mesh, 4, False, ops_seed=8, lam=0.3,
+             bubble=(0.5, (8_000.0, 8_000.0, 200.0), (4000.0, 4000.0, 100.0)),
+             C=15.0, nsteps=10, keep=(1, 10), set_name="set2c")
     with open(os.path.join(HERE, "HOST.json"), "w") as f:
         json.dump(host, f, indent=1)
 

@@ -47,9 +47,9 @@ def test_library_rejects_bad_plan_arguments_without_gpu():
     lib = _native.load()
     gd = _native.GridDesc(nex=2, ney=2, nez=2, N=9, Ny=9, slab=0, x0=0, y0=0, lX=19, lY=19,
                           px=20, ex_b=0, ex_e=2, ey_b=0, ey_e=2)
-    arrs = [np.zeros(64) for _ in range(16)]
+    arrs = [np.zeros(64) for _ in range(18)]
     rd = _native.RefDesc(*[a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) for a in arrs],
-                         9.8, 287.0, 1e5, 1.4)
+                         9.8, 287.0, 1e5, 1.4, 0)
     h = ctypes.c_void_p()
     rc = lib.hevi_plan_create(ctypes.byref(h), ctypes.byref(gd), ctypes.byref(rd))
     assert rc == -1 and b"order" in lib.hevi_last_error()
@@ -72,7 +72,7 @@ def test_unsupported_paths_raise_not_implemented():
     disc = euler.build_discretization(mesh)
     q = np.zeros((5,) + mesh.nshape)
     with pytest.raises(NotImplementedError):
-        euler.nonlinear_rhs(q, ref, disc, "set2c")
+        euler.nonlinear_rhs(q, ref, disc, "set2c", dg=True)
     with pytest.raises(ValueError):
         euler.nonlinear_rhs(q, ref, disc, "set3")
     with pytest.raises(NotImplementedError):
