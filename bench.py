@@ -225,16 +225,17 @@ def run_gpu(args):
                                       cfg["Lz"], cfg["N"])
     ref = euler.hydrostatic_reference(mesh, 300.0)
     disc = euler.build_discretization(mesh)
-    q0 = cases.bubble_lattice(mesh, ref, 0.5, cfg["centre"], cfg["radii"])
+    sn = args.set
+    q0 = cases.bubble_lattice(mesh, ref, 0.5, cfg["centre"], cfg["radii"], set_name=sn)
     courant = args.courant if args.courant else cfg["courant"]
-    dt = cases.dt_for_courant(mesh, ref, q0, courant)
+    dt = cases.dt_for_courant(mesh, ref, q0, courant, sn)
     tab = imexcore.ark2_tableau()
     lam = tab.diag * dt
     n_unique = mesh.n_unique
     dof = 5 * n_unique
 
     if world == 1:
-        plan = disc.plan_for(ref)
+        plan = disc.plan_for(ref, sn)
         plan.factor(lam)
         Q = plan.zeros()
         Q[..., :mesh.X].copy_(q0)
@@ -244,7 +245,7 @@ def run_gpu(args):
     else:
         from paper_1702_04316_b200.distributed import DistributedStepper, grid_for
         px, py = grid_for(world)
-        ds = DistributedStepper(mesh, ref, disc, dt, px, py, rank)
+        ds = DistributedStepper(mesh, ref, disc, dt, px, py, rank, set_name=sn)
         ds.load_global(q0)
         plan, Q, work, exch = ds.plan, ds.Q, ds.work, ds.exchange
     del q0
@@ -394,6 +395,7 @@ def run_gpu(args):
                           "columns": mesh.n_col, "levels": mesh.n_lev, "dt_s": dt,
                           "parallelism": f"columns {px}x{py}",
                           "integrator": args.integrator, "courant_v": courant,
+                          "equation_set": sn,
                           "sim_seconds_per_wall_second": dt / (ms_step * 1e-3),
                           "l2": "inputs larger than L2 (state %.0f MB vs 126 MB L2)"
                                 % (8 * dof / 1e6)},
@@ -412,9 +414,9 @@ def run_e2e(args, mesh, ref, disc, dt, tab, plan, Q, work, exch, world, rank, do
     from paper_1702_04316_b200 import imexcore, euler
     from paper_1702_04316_b200.plan import tableau_array
     if world == 1:
-        prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d",
+        prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name=args.set, dim="1d",
                                         solver=imexcore.SolverSpec(method="direct"))
-        rhs = euler.make_rhs(ref, disc, "set2nc")
+        rhs = euler.make_rhs(ref, disc, args.set)
         host = torch.empty((5,) + tuple(mesh.nshape), dtype=torch.float64, pin_memory=True)
         host.copy_(plan.l2e(Q))
         torch.cuda.synchronize()
@@ -475,6 +477,8 @@ def main():
     ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
     ap.add_argument("--integrator", default="ark2", choices=["ark2", "rk35"],
                     help="ark2: HEVI 1D-IMEX (the metric); rk35: explicit reference (config 2)")
+    ap.add_argument("--set", default="set2nc", choices=["set2nc", "set2c"],
+                    help="equation set (set2nc: the reference's default)")
     ap.add_argument("--courant", type=float, default=0.0, help="override the config's C_V")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

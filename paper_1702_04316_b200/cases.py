@@ -13,8 +13,9 @@ import numpy as np
 
 
 def bubble_lattice(mesh, ref, theta_c=0.5, centre=None, radii=(250.0, 250.0, 250.0),
-                   device="cuda"):
-    """(5, Z, Y, X) fp64 tensor: cosine theta' bump, rho' for zero P'."""
+                   device="cuda", set_name="set2nc"):
+    """(5, Z, Y, X) fp64 tensor: cosine theta' bump, rho' for zero P'.
+    set2c: Theta' = 0 (rho theta unchanged, so P' = 0), as bench.py:118-123."""
     import torch
     if centre is None:
         centre = (0.5 * mesh.Lx, 0.5 * mesh.Ly, 350.0)
@@ -28,7 +29,8 @@ def bubble_lattice(mesh, ref, theta_c=0.5, centre=None, radii=(250.0, 250.0, 250
     theta0 = torch.as_tensor(ref.theta0, device=device)[:, None, None]
     q = torch.zeros((5, mesh.Z, mesh.Y, mesh.X), dtype=torch.float64, device=device)
     q[0] = rho0 * (theta0 / (theta0 + th) - 1.0)
-    q[4] = th
+    if set_name != "set2c":
+        q[4] = th
     return q
 
 

@@ -1,22 +1,47 @@
-import sys, numpy as np, torch
+"""Parity table of the CUDA path (run on a B200): per case, relative L2 errors
+(rho', |vel|, theta') of R, L_V, the Schur solve and 10 ARK2 steps against the
+reference goldens and against the oracle with cancellation-free P'
+(pprime="exact").  Output goes to stdout; profiles/parity_r01.txt keeps a copy."""
+import sys
 sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
-from conftest import CASES, load_golden, oracle_for, rel_fields
-from test_gpu_parity import build, dev
-from paper_1702_04316_b200 import euler, imexcore
+from conftest import CASES, load_golden, oracle_for, rel_fields, set_of  # noqa: E402
+from test_gpu_parity import build, dev  # noqa: E402
+from paper_1702_04316_b200 import euler, imexcore  # noqa: E402
+
+
+def fmt(e):
+    return "[" + ", ".join("%.1e" % x for x in e) + "]"
+
+
+print("case            set     quantity       vs reference golden        vs exact-P' oracle")
 for name in sorted(CASES):
-    mesh, ref, disc = build(name); o = oracle_for(name); g = load_golden(name)
+    sn = set_of(name)
+    mesh, ref, disc = build(name)
+    o, ox, g = oracle_for(name), oracle_for(name, "exact"), load_golden(name)
     q = o.from_lattice(g["ops_q"])
-    R = euler.nonlinear_rhs(dev(q), ref, disc, "set2nc").cpu().numpy()
-    print(name, "R", ["%.2e" % e for e in rel_fields(o.to_lattice(R), g["ops_R"])])
-    L = euler.vertical_restriction(dev(q), ref, disc, "set2nc").cpu().numpy()
-    print(name, "L", ["%.2e" % e for e in rel_fields(o.to_lattice(L), g["ops_L"])])
-    p = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d", solver=imexcore.SolverSpec(method="direct")); p.lam = float(g["ops_lam"])
-    S = p.solve(dev(q)).cpu().numpy()
-    print(name, "S", ["%.2e" % e for e in rel_fields(o.to_lattice(S), g["ops_solve"])])
-    qq = dev(o.from_lattice(g["step_q0"])); dt = float(g["step_dt"]); qo = o.from_lattice(g["step_q0"])
-    keep = sorted(int(k[6:]) for k in g.files if k.startswith("step_q") and k != "step_q0")
-    rhs = euler.make_rhs(ref, disc, "set2nc"); tab = imexcore.ark2_tableau()
-    for k in range(1, keep[-1]+1):
+    lam = float(g["ops_lam"])
+    p = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name=sn, dim="1d",
+                                 solver=imexcore.SolverSpec(method="direct"))
+    p.lam = lam
+    rows = [
+        ("R", euler.nonlinear_rhs(dev(q), ref, disc, sn), g["ops_R"], ox.rhs(q)),
+        ("L_V", euler.vertical_restriction(dev(q), ref, disc, sn), g["ops_L"], ox.linear(q)),
+        ("solve", p.solve(dev(q)), g["ops_solve"], ox.solve(q, lam)),
+    ]
+    for tag, got, want, wx in rows:
+        got = o.to_lattice(got.cpu().numpy())
+        print(f"{name:15s} {sn:7s} {tag:14s} {fmt(rel_fields(got, want)):26s} "
+              f"{fmt(rel_fields(got, ox.to_lattice(wx)))}")
+    q0 = o.from_lattice(g["step_q0"])
+    qq, qx = dev(q0), q0.copy()
+    dt = float(g["step_dt"])
+    rhs = euler.make_rhs(ref, disc, sn)
+    tab = imexcore.ark2_tableau()
+    for k in range(1, 11):
         qq = imexcore.ark_imex_step(qq, dt, tab, p, rhs)
-        if k in keep:
-            print(name, "step", k, "vs ref", ["%.2e" % e for e in rel_fields(o.to_lattice(qq.cpu().numpy()), g[f"step_q{k}"])])
+        qx = ox.step(qx, dt)
+        if f"step_q{k}" in g.files:
+            got = o.to_lattice(qq.cpu().numpy())
+            print(f"{name:15s} {sn:7s} {'step %d' % k:14s} "
+                  f"{fmt(rel_fields(got, g[f'step_q{k}'])):26s} "
+                  f"{fmt(rel_fields(got, ox.to_lattice(qx)))}")
