@@ -127,6 +127,29 @@ int hevi_flags(hevi_plan *plan, unsigned *flags, int reset, void *stream);
  *                  *bad_col receives the first degenerate column or -1
  * hevi_band_solve: columnsolve.solve_columns_direct (:156-181), rhs (n_col, M)
  *                  row-major, solved in place                                  */
+/* Run diagnostics (bench.total_mass / max_perturbations, bench.py:131-137) of a
+ * lattice state of this plan: out_host[0] = sum_g Wx[gx] Wy[gy] Wz[gz] (rho0 +
+ * rho'), out_host[1] = max |rho'|, out_host[2] = max |q4|; Wx/Wy/Wz are the
+ * per-axis unique-point quadrature weights (device arrays of X, Y, Z). */
+int hevi_diagnostics(const hevi_plan *plan, const double *q, const double *wx, const double *wy,
+                     const double *wz, double *out_host, void *stream);
+
+/* columnsolve.factor_with_fallback (columnsolve.py:141-153) pivoted path:
+ * hevi_lu_pivot:       batched in-place partial-pivoting LU of (n_col, M, M)
+ *                      row-major matrices (scipy.linalg.lu_factor / getrf:
+ *                      piv[c*M+k] = row interchanged with k, 0-based;
+ *                      info_host[c] = k+1 for the first exactly-zero pivot)
+ * hevi_lu_pivot_solve: scipy.linalg.lu_solve per column, rhs (n_col, M) in place */
+int hevi_lu_pivot(double *A, int *piv, int n_col, int M, int *info_host, void *stream);
+int hevi_lu_pivot_solve(const double *LU, const int *piv, double *rhs, int n_col, int M, void *stream);
+
+/* plan options; HEVI_OPT_FORCE_PIVOTED makes hevi_factor keep the pivoted
+ * dense factor even when the no-pivot LU succeeds (exercises the fallback) */
+#define HEVI_OPT_FORCE_PIVOTED 1
+int hevi_plan_set_option(hevi_plan *plan, int option, int value);
+/* whether the factor of lam took the pivoted fallback (columnsolve.py:150-152) */
+int hevi_factor_pivoted(const hevi_plan *plan, double lam, int *pivoted);
+
 int hevi_band_pack(const double *dense, double *band, int n_col, int M, int nb, void *stream);
 int hevi_band_unpack(const double *band, double *dense, int n_col, int M, int nb, void *stream);
 int hevi_band_lu(double *band, int n_col, int M, int nb, double norm, int *bad_col, void *stream);

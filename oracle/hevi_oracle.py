@@ -552,12 +552,32 @@ class BoxOracle:
             y[:, i] /= LU[:, i, i]
         return y
 
-    def factors(self, lam):
-        """columnsolve.get_factors cache keyed by round(lam, 12) (:184-188)."""
-        key = round(lam, 12)
+    @staticmethod
+    def pivoted_factors(A):
+        """factor_with_fallback's pivoted dense path (columnsolve.py:148-152):
+        scipy.linalg.lu_factor per column."""
+        import scipy.linalg
+        return [scipy.linalg.lu_factor(A[c]) for c in range(A.shape[0])]
+
+    @staticmethod
+    def pivoted_solve(F, rhs):
+        """solve_columns_direct's pivoted branch (columnsolve.py:163-167)."""
+        import scipy.linalg
+        return np.stack([scipy.linalg.lu_solve(F[c], rhs[c]) for c in range(rhs.shape[0])])
+
+    def factors(self, lam, force_pivoted=False):
+        """columnsolve.get_factors cache keyed by round(lam, 12) (:184-188),
+        factor_with_fallback (:141-153): (LU, nb) or ("pivoted", factors)."""
+        key = (round(lam, 12), force_pivoted)
         if key not in self._column_cache:
             A, nb = self.column_matrices(lam)
-            self._column_cache[key] = (self.band_lu(A, nb), nb)
+            backup = A.copy()
+            try:
+                if force_pivoted:
+                    raise RuntimeError("forced")
+                self._column_cache[key] = (self.band_lu(A, nb), nb)
+            except RuntimeError:
+                self._column_cache[key] = ("pivoted", self.pivoted_factors(backup))
         return self._column_cache[key]
 
     def solve(self, qe, lam):
@@ -565,10 +585,13 @@ class BoxOracle:
         columnsolve.solve_direct (columnsolve.py:191-210)."""
         if lam <= 0:
             raise ValueError("implicit solve requires positive lam")
-        LU, nb = self.factors(lam)
+        LU, nb = self.factors(lam, getattr(self, "force_pivoted", False))
         rhsP, ua = self.schur_rhs(qe, lam)
         rhs = rhsP.ravel()[self.rep].reshape(self.n_col, self.n_lev)
-        sol = self.band_solve(LU, nb, rhs)
+        if isinstance(LU, str):
+            sol = self.pivoted_solve(nb, rhs)
+        else:
+            sol = self.band_solve(LU, nb, rhs)
         P = sol.reshape(-1)[self.uid].reshape(self.nshape)
         return self.extract(P, ua, qe, lam)
 

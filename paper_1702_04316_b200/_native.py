@@ -69,6 +69,11 @@ SIGNATURES = {
     "hevi_band_lu": (_I, [_V, _I, _I, _I, _D, ctypes.POINTER(_I), _V]),
     "hevi_band_solve": (_I, [_V, _V, _I, _I, _I, _V]),
     "hevi_absmax": (_I, [_V, _LL, ctypes.POINTER(_D), _V]),
+    "hevi_lu_pivot": (_I, [_V, _V, _I, _I, _V, _V]),
+    "hevi_diagnostics": (_I, [_V, _V, _V, _V, _V, _V, _V]),
+    "hevi_lu_pivot_solve": (_I, [_V, _V, _V, _I, _I, _V]),
+    "hevi_plan_set_option": (_I, [_V, _I, _I]),
+    "hevi_factor_pivoted": (_I, [_V, _D, ctypes.POINTER(_I)]),
 }
 
 _lib = None

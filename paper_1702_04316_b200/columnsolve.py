@@ -73,6 +73,9 @@ class ColumnJacobian:
     pivoted_fallback: list = None
     piv: dict = None
     band: object = None          # device band storage after factoring
+    lu: object = None            # pivoted fallback: (n_col, M, M) LU factors
+    lu_piv: object = None        # pivoted fallback: (n_col, M) int32 interchanges
+    lu_info: object = None       # pivoted fallback: getrf-style info per column
 
     @property
     def M(self) -> int:
@@ -143,12 +146,39 @@ def _band_mask(M, nb, device):
     return ((i[:, None] - i[None, :]).abs() < nb)[None]
 
 
+def lu_factor_pivoted(cj: ColumnJacobian):
+    """The pivoted dense fallback of factor_with_fallback (columnsolve.py:148-152):
+    partial-pivoting LU of every column on the device (scipy.linalg.lu_factor
+    semantics); ``cj.piv[c] = (lu, piv)`` per column like the reference."""
+    import torch
+    lib = nv.load()
+    A = cj.matrices
+    if not isinstance(A, torch.Tensor) or not A.is_cuda:
+        A = torch.as_tensor(np.asarray(A, dtype=np.float64), device="cuda")
+    lu = A.to(torch.float64).contiguous().clone()
+    n_col, M, _ = lu.shape
+    piv = torch.empty((n_col, M), dtype=torch.int32, device=lu.device)
+    info = np.zeros(n_col, dtype=np.int32)
+    nv.check(lib.hevi_lu_pivot(nv.ptr(lu), nv.ptr(piv), n_col, M,
+                               info.ctypes.data_as(ctypes.c_void_p), nv.stream_ptr()))
+    cj.lu, cj.lu_piv, cj.lu_info = lu, piv, info
+    cj.piv = {c: (lu[c], piv[c]) for c in range(n_col)}
+    cj.pivoted_fallback = list(range(n_col))
+    cj.factored = True
+    return cj
+
+
 def factor_with_fallback(problem) -> ColumnJacobian:
-    """columnsolve.py:141-153.  The pivoted dense fallback is not ported
-    (no-pivot LU never falls back on the Schur columns, SURVEY finding 5):
-    a degenerate pivot raises."""
+    """columnsolve.py:141-153: build and factor, keeping a pivoted dense LU of
+    every column if the no-pivot banded LU hits a degenerate diagonal.  The
+    fused step's shared factor takes the same fallback inside hevi_factor."""
     cj = build_column_jacobian(problem)
-    lu_factor_banded(cj)
+    backup = cj.matrices.clone()
+    try:
+        lu_factor_banded(cj)
+    except RuntimeError:
+        cj.matrices = backup
+        lu_factor_pivoted(cj)
     return cj
 
 
@@ -164,6 +194,10 @@ def solve_columns_direct(cj: ColumnJacobian, rhs):
     dev = t.device
     x = t.to(device="cuda", dtype=torch.float64).contiguous().clone()
     n_col, M = x.shape
+    if cj.pivoted_fallback:    # columnsolve.py:163-167
+        nv.check(lib.hevi_lu_pivot_solve(nv.ptr(cj.lu), nv.ptr(cj.lu_piv), nv.ptr(x), n_col, M,
+                                         nv.stream_ptr()))
+        return x.cpu().numpy() if was_np else x.to(dev)
     nv.check(lib.hevi_band_solve(nv.ptr(cj.band), nv.ptr(x), n_col, M, int(cj.bandwidth),
                                  nv.stream_ptr()))
     if was_np:

@@ -3,13 +3,15 @@
 //
 // One CTA per horizontal tile of TX x TY element columns sweeps the element
 // layers bottom-up.  Per layer:
-//   1. TMA (cp.async.bulk.tensor, 4D box x,y,z,field) brings the layer's
-//      N+1 levels of the 5 input fields for the tile plus its low-side halo
-//      into a staging buffer; the load of layer ez+1 is issued right after
-//      layer ez has been converted, so it runs underneath layer ez's compute;
-//   2. the staged levels are converted into a ring buffer of N+1 level slots
-//      (the top level of a layer is the bottom of the next): the 5 fields,
-//      P' and the linearised pressure.  P' = EOS(rho, theta) - P0f
+//   1. TMA (cp.async.bulk.tensor, 4D box x,y,1 level,5 fields) writes each
+//      new level of the tile plus its low-side halo straight into its slot of
+//      a ring of 2N+1 level slots (the top level of a layer is the bottom of
+//      the next).  Two layers are resident: while layer ez computes, the N
+//      levels of layer ez+1 are in flight, issued at the end of layer ez-1
+//      (two mbarriers, one per layer parity), so a load has a whole layer of
+//      compute to land and nothing is copied between shared buffers;
+//   2. P' of the layer's new levels is formed in place (6th plane of the
+//      slot).  P' = EOS(rho, theta) - P0f
 //      (euler.py:454-457) is evaluated as Pb (1+delta)^gamma - P0f with
 //      delta = (rho theta - rho0 theta0)/(rho0 theta0) by its binomial series
 //      (15 terms, |delta| <= 1/8; exact pow beyond): the same function,
@@ -35,22 +37,27 @@ struct E2 {
     // illegal TMA request on sm_100a; tools/tma_probe.cu)
     static constexpr int LXT = (LX + 2) / 2 * 2;
     static constexpr int LY = TY * NY + NY + 1;
-    static constexpr int NL = N + 1;                          // level slots (ring)
-    static constexpr int PL = LY * LXT;                       // one level plane
+    static constexpr int NL = N + 1;                          // levels per layer
+    static constexpr int RING = 2 * N + 1;                    // level slots (two layers)
+    static constexpr int PL = LY * LXT;                       // one field plane of a level
+    static constexpr int SS = (6 * PL + 15) / 16 * 16;        // slot stride (128-byte aligned)
+#ifdef HEVI_X_K
+    static constexpr int K = HEVI_X_K;
+#else
     static constexpr int K = (N % 2 == 0) ? 2 : 1;             // vertical points per thread
+#endif
     static constexpr int NT = OX * OYM * (N / K);             // main threads
     static constexpr int BLK = (NT + 31) / 32 * 32;
     static constexpr int CXW = OX + 1, CYW = TY * NY + 1 + (NY == 1 ? 1 : 0);
-    static constexpr int STG_N = 5 * NL * PL;                 // TMA staging
-    static constexpr int S_N = 6 * NL * PL;                   // ring: rho', u, v, w, theta', P'
+    static constexpr int S_N = RING * SS;                     // ring: rho', u, v, w, theta', P'
     static constexpr int CAR_N = 2 * 7 * CYW * CXW;           // double-buffered carry
     static constexpr int XF_N = 6 * TX * OYM * N;             // x-face partials
     static constexpr int DN = (N + 1) * (N + 1), DNY = (NY + 1) * (NY + 1);
     static constexpr size_t fixed_bytes() {
-        return sizeof(double) * (size_t)(STG_N + S_N + CAR_N + XF_N + DN + DNY + 1) + 128;
+        return sizeof(double) * (size_t)(S_N + CAR_N + XF_N + DN + DNY + 2) + 128;
     }
     static constexpr int NTAB = 12;                           // level tables in smem
-    static constexpr uint32_t TMA_BYTES = (uint32_t)(sizeof(double) * STG_N);
+    static constexpr uint32_t LVL_BYTES = (uint32_t)(sizeof(double) * 5 * PL);   // one level TMA
 };
 
 // smem level tables
@@ -144,7 +151,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                                        int oz0, int ox, int oy, int gx, int gy, int ez, double cx,
                                        double cy, int Z) {
     using T = E2<N, NY, TX, TY>;
-    constexpr int PL = T::PL, LXT = T::LXT, NL = T::NL;
+    constexpr int PL = T::PL, LXT = T::LXT, RING = T::RING, SS = T::SS;
     constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
     constexpr bool NEED_R = (MODE != M_L);
     const Geo& g = a.g;
@@ -156,7 +163,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
     for (int k = 0; k < K; ++k) {
         gzk[k] = base + oz0 + k;
         o[k] = loff(g, gx, gy, gzk[k]);
-        sl[k] = (base + oz0 + k) % NL;
+        sl[k] = (base + oz0 + k) % RING;
     }
     // stage inputs read pointwise: issue early, consume in the epilogue
     double Ain[K][5], Fin[K][5];
@@ -173,21 +180,22 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
     }
     int zs[N + 1];
 #pragma unroll
-    for (int m = 0; m <= N; ++m) zs[m] = ((base + m) % NL) * PL;
+    for (int m = 0; m <= N; ++m) zs[m] = ((base + m) % RING) * SS;
     const int cidx = oy * T::CXW + ox;
-    const bool do_carry = (oz0 == 0) && (ez + 1 < g.nez);
+    const bool more = ez + 1 < g.nez;
+    const bool do_carry = (oz0 == 0) && more;
     const bool zface = (oz0 == 0) && (ez > 0);
-    const double* Sxy = S + ay.l * LXT + ax.l;   // column base (plus f*NL*PL + slot*PL)
+    const double* Sxy = S + ay.l * LXT + ax.l;   // column base (plus slot*SS + f*PL)
 
     double r[K], u[K], v[K], w[K], th[K], rho[K], rinv[K], cz[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const double* pp = Sxy + sl[k] * PL;
-        r[k] = pp[0 * NL * PL];
-        u[k] = pp[1 * NL * PL];
-        v[k] = pp[2 * NL * PL];
-        w[k] = pp[3 * NL * PL];
-        th[k] = pp[4 * NL * PL];
+        const double* pp = Sxy + sl[k] * SS;
+        r[k] = pp[0 * PL];
+        u[k] = pp[1 * PL];
+        v[k] = pp[2 * PL];
+        w[k] = pp[3 * PL];
+        th[k] = pp[4 * PL];
         rho[k] = LT[gzk[k] * T::NTAB + T_RHO0] + r[k];
         rinv[k] = 1.0 / rho[k];
         cz[k] = LT[gzk[k] * T::NTAB + T_CZ];
@@ -195,17 +203,17 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
     // d/dx, d/dy, d/dz of field f at the K points (DSS-averaged, folded)
     // per-layer line base addresses: every line load below is base + a
     // compile-time offset (field * SF + m * stride)
-    constexpr int SF = NL * PL;
+    constexpr int SF = PL;
     const double* bx_[K];
     const double* bxl_[K];
     const double* by_[K];
     const double* byl_[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        bx_[k] = S + sl[k] * PL + ay.l * LXT + ax.s0;
-        bxl_[k] = S + sl[k] * PL + ay.l * LXT + ax.l - N;
-        by_[k] = S + sl[k] * PL + ay.s0 * LXT + ax.l;
-        byl_[k] = S + sl[k] * PL + (ay.l - NY) * LXT + ax.l;
+        bx_[k] = S + sl[k] * SS + ay.l * LXT + ax.s0;
+        bxl_[k] = S + sl[k] * SS + ay.l * LXT + ax.l - N;
+        by_[k] = S + sl[k] * SS + ay.s0 * LXT + ax.l;
+        byl_[k] = S + sl[k] * SS + (ay.l - NY) * LXT + ax.l;
     }
     const double* bz_[N + 1];
 #pragma unroll
@@ -271,7 +279,11 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
             }
             gzv[k] = cz[k] * d;
         }
-        if (do_carry) {
+        // the top-face carries of a column are split over its z-groups by field
+        // (warp-uniform: the group index is the slowest thread coordinate)
+        constexpr int NG = N / K;
+        const bool carry_f = (MAIN && NG > 1) ? (more && (f % NG) == oz0 / K) : do_carry;
+        if (carry_f) {
             double top = 0.0;
 #pragma unroll
             for (int m = 0; m <= N; ++m) top = fma(sDx[N * (N + 1) + m], val[m], top);
@@ -419,23 +431,23 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
     }
 }
 
+// fallback staging without TMA: level z0 of the tile (+halo) into a ring
+// slot, same placement (x shifted by xsh) and zero fill as the TMA
 template <int N, int NY, int TX, int TY>
-__device__ __forceinline__ void stage_manual(double* STG, const EArgs& a, int tx0, int ty0, int z0) {
+__device__ __forceinline__ void stage_level_manual(double* slot, const EArgs& a, int tx0, int ty0, int z0) {
     using T = E2<N, NY, TX, TY>;
     const Geo& g = a.g;
-    constexpr int TOT = 5 * T::NL * T::LY * T::LXT;
+    constexpr int TOT = 5 * T::PL;
     for (int i = threadIdx.x; i < TOT; i += T::BLK) {
         const int x = i % T::LXT;
-        int t = i / T::LXT;
+        const int t = i / T::LXT;
         const int y = t % T::LY;
-        t /= T::LY;
-        const int z = t % T::NL;
-        const int f = t / T::NL;
-        const int ix = tx0 + x, iy = ty0 + y, iz = z0 + z;
+        const int f = t / T::LY;
+        const int ix = tx0 + x, iy = ty0 + y;
         double v = 0.0;
-        if (ix >= 0 && ix < g.lX && iy >= 0 && iy < g.lY && iz < g.Z)
-            v = a.q[f * g.fs + ((long long)iz * g.lY + iy) * g.px + ix];
-        STG[i] = v;
+        if (ix >= 0 && ix < g.lX && iy >= 0 && iy < g.lY && z0 < g.Z)
+            v = a.q[f * g.fs + ((long long)z0 * g.lY + iy) * g.px + ix];
+        slot[i] = v;
     }
 }
 
@@ -443,22 +455,19 @@ template <int N, int NY, int TX, int TY, int MODE, int MINB>
 __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     k_explicit2(const EArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T = E2<N, NY, TX, TY>;
-    constexpr int PL = T::PL, LXT = T::LXT, NL = T::NL, BLK = T::BLK;
-    constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
+    constexpr int PL = T::PL, LXT = T::LXT, RING = T::RING, SS = T::SS, BLK = T::BLK;
     constexpr bool NEED_R = (MODE != M_L);
     extern __shared__ __align__(128) unsigned char smraw[];
     // TMA destinations must be 128-byte aligned: align the carve-up explicitly
     double* smd = reinterpret_cast<double*>(
         smraw + ((128u - ((unsigned)__cvta_generic_to_shared(smraw) & 127u)) & 127u));
-    double* STG = smd;
-    double* S = STG + T::STG_N;
-    double* CAR = S + T::S_N;
+    double* Sa = smd;                 // ring, 128-byte aligned slots (TMA destinations)
+    double* CAR = Sa + T::S_N;
     double* XF = CAR + T::CAR_N;
     double* sDx = XF + T::XF_N;
     double* sDy = sDx + T::DN;
     double* LT = sDy + T::DNY;
-    uint64_t* mbarp = reinterpret_cast<uint64_t*>(LT + T::NTAB * a.g.Z);
-    uint64_t& mbar = *mbarp;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(LT + T::NTAB * a.g.Z);   // [2], per layer parity
     const Geo& g = a.g;
     const int Z = g.Z;
     const int tid = threadIdx.x;
@@ -473,7 +482,8 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     const int gxlo = (ex0 - 1) * N, gylo = (ey0 - 1) * NY;
 
     if (tid == 0) {
-        mbar_init(&mbar, 1);
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
     }
     for (int i = tid; i < T::DN; i += BLK) sDx[i] = a.Dx[i];
@@ -497,23 +507,24 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     const int txr = gxlo - g.x0, ty0 = gylo - g.y0;
     const int xsh = txr & 1;          // staged column of lx is lx + xsh
     const int tx0 = txr - xsh;
+    double* S = Sa + xsh;             // compute view: column lx at S[... + lx]
     const bool use_tma = a.use_tma != 0;
-    if (use_tma) {
-        if (tid == 0) {
-            mbar_expect_tx(&mbar, T::TMA_BYTES);
-            tma_load_4d(STG, &tmap, &mbar, tx0, ty0, 0, 0);
+    // layers 0 and 1 in flight before the sweep starts (levels 0..2N, slots 0..2N)
+    if (use_tma && tid == 0) {
+        mbar_expect_tx(&mbar[0], (N + 1) * T::LVL_BYTES);
+        for (int l = 0; l <= N; ++l) tma_load_4d(Sa + l * SS, &tmap, &mbar[0], tx0, ty0, l, 0);
+        if (g.nez > 1) {
+            mbar_expect_tx(&mbar[1], N * T::LVL_BYTES);
+            for (int l = N + 1; l <= 2 * N; ++l) tma_load_4d(Sa + l * SS, &tmap, &mbar[1], tx0, ty0, l, 0);
         }
-    } else {
-        stage_manual<N, NY, TX, TY>(STG, a, tx0, ty0, 0);
-        __syncthreads();
     }
 
     // ---- the thread's main points (fixed for the whole sweep) -------------
     constexpr int K = T::K;
     const bool has_main = tid < T::NT;
     const int mox = tid % T::OX;
-    const int mop = (tid / T::OX) % (N / K);
-    const int moy = tid / (T::OX * (N / K));
+    const int moy = (tid / T::OX) % T::OYM;
+    const int mop = tid / (T::OX * T::OYM);      // z-group: warp-uniform
     const int moz = mop * K;
     const bool main_ok = has_main && mox < oxm && moy < oym;
     const int mgx = ex0 * N + mox, mgy = ey0 * NY + moy;
@@ -545,54 +556,38 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
 #endif
     for (int ez = 0; ez < g.nez; ++ez) {
         const int base = ez * N;
-        // ---------------- 1. staged layer -> ring slots ---------------------
-        if (use_tma) mbar_wait(&mbar, ez & 1);
-        PH(0);
+        // ---------------- 1. this layer's new levels, P' in place -----------
         const int lz0 = (ez == 0) ? 0 : 1;
-        const int nconv = (NL - lz0) * T::LY * T::LX;
-        for (int idx = tid; idx < nconv; idx += BLK) {
-            const int lx = idx % T::LX;
-            const int t = idx / T::LX;
-            const int ly = t % T::LY;
-            const int lz = lz0 + t / T::LY;
-            const int gz = base + lz;
-            const int st = (lz * T::LY + ly) * LXT + lx + xsh;
-            const double r = STG[0 * NL * PL + st], u = STG[1 * NL * PL + st],
-                         v = STG[2 * NL * PL + st], w = STG[3 * NL * PL + st],
-                         th = STG[4 * NL * PL + st];
-            double pp = 0.0;
-            if (NEED_R)
-                pp = pprime(r, th, LT[(gz) * T::NTAB + T_RHO0], LT[(gz) * T::NTAB + T_TH0], LT[(gz) * T::NTAB + T_E0],
-                            LT[(gz) * T::NTAB + T_C0], LT[(gz) * T::NTAB + T_IRT0], LT[(gz) * T::NTAB + T_P0F], bc, a.ph);
-            const int d = ((gz % NL) * T::LY + ly) * LXT + lx;
-            S[0 * NL * PL + d] = r;
-            S[1 * NL * PL + d] = u;
-            S[2 * NL * PL + d] = v;
-            S[3 * NL * PL + d] = w;
-            S[4 * NL * PL + d] = th;
-            S[5 * NL * PL + d] = pp;
+        if (use_tma) {
+            mbar_wait(&mbar[ez & 1], (ez >> 1) & 1);
+        } else {
+            for (int lz = lz0; lz <= N; ++lz)
+                stage_level_manual<N, NY, TX, TY>(Sa + ((base + lz) % RING) * SS, a, tx0, ty0, base + lz);
+            __syncthreads();
+        }
+        PH(0);
+        if (NEED_R) {
+            const int nconv = (N + 1 - lz0) * T::LY * T::LX;
+            for (int idx = tid; idx < nconv; idx += BLK) {
+                const int lx = idx % T::LX;
+                const int t = idx / T::LX;
+                const int ly = t % T::LY;
+                const int gz = base + lz0 + t / T::LY;
+                double* sp = S + (gz % RING) * SS + ly * LXT + lx;
+                const double* lt = LT + gz * T::NTAB;
+                sp[5 * PL] = pprime(sp[0], sp[4 * PL], lt[T_RHO0], lt[T_TH0], lt[T_E0], lt[T_C0],
+                                    lt[T_IRT0], lt[T_P0F], bc, a.ph);
+            }
         }
         PH(1);
         __syncthreads();
         PH(2);
-        // the staging buffer is free: fetch the next layer under this layer's compute
-        if (use_tma) {
-            if (tid == 0 && ez + 1 < g.nez) {
-                // generic-proxy reads of STG are ordered before the async-proxy refill
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&mbar, T::TMA_BYTES);
-                tma_load_4d(STG, &tmap, &mbar, tx0, ty0, base + N, 0);
-            }
-        } else if (ez + 1 < g.nez) {
-            stage_manual<N, NY, TX, TY>(STG, a, tx0, ty0, base + N);
-            // (the barrier after the partial sums orders these writes before use)
-        }
         // ---------------- 2. shared partial sums ----------------------------
         double* CARw = CAR + (ez & 1) * (7 * T::CYW * T::CXW);
         const double* CARr = CAR + ((ez + 1) & 1) * (7 * T::CYW * T::CXW);
         {
             // row N of the left element at the tile's element x-faces
-            constexpr int NXF = 6 * TX * T::OYM * N;
+            constexpr int NXF = T::XF_N;
             for (int it = tid; it < NXF; it += BLK) {
                 const int oz = it % N;
                 int t = it / N;
@@ -600,7 +595,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                 t /= T::OYM;
                 const int ae = t % TX;
                 const int f = t / TX;
-                const double* sx = S + f * (NL * PL) + ((base + oz) % NL) * PL + (oy + NY) * LXT + ae * N;
+                const double* sx = S + f * PL + ((base + oz) % RING) * SS + (oy + NY) * LXT + ae * N;
                 double s = 0.0;
 #pragma unroll
                 for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sx[m], s);
@@ -645,6 +640,16 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
         PH(5);
         __syncthreads();
         PH(6);
+        // levels base .. base+N-1 are dead: refill their slots with layer ez+2
+        if (use_tma && tid == 0 && ez + 2 < g.nez) {
+            // generic-proxy accesses of the slots are ordered before the async-proxy refill
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&mbar[ez & 1], N * T::LVL_BYTES);
+            for (int l = 1; l <= N; ++l) {
+                const int L = base + 2 * N + l;
+                tma_load_4d(Sa + (L % RING) * SS, &tmap, &mbar[ez & 1], tx0, ty0, L, 0);
+            }
+        }
     }
 #ifdef HEVI_PHASE_TIMING
     if (a.dbg) {

@@ -19,6 +19,13 @@
 //    (box meshes: all columns identical), extraction -- fused.
 #include "../../include/hevi.h"
 
+// experiment builds: -DHEVI_DEV_N=4 instantiates one polynomial order only
+// (every dispatch case maps to it; never used for the shipped library)
+#ifdef HEVI_DEV_N
+#define DN(n) HEVI_DEV_N
+#else
+#define DN(n) n
+#endif
 #ifndef HEVI_T44_TX
 #define HEVI_T44_TX 4
 #endif
@@ -730,7 +737,7 @@ __global__ void k_lu_dense(double* A, double* LU, double* LUb, int M, int* nb_ou
     for (int k = 0; k < M; ++k) {
         double piv = LU[k * M + k];
         if (fabs(piv) < 1e-12 * norm) {
-            if (tid == 0) atomicOr(flags, HEVI_F_PIVOT);
+            if (tid == 0) atomicOr(flags, 1u);   // degenerate: the plan falls back to pivoted LU
             piv = 1.0;
         }
         const int E = min(k + nb, M);
@@ -757,6 +764,159 @@ __global__ void k_lu_dense(double* A, double* LU, double* LUb, int M, int* nb_ou
     }
     for (int k = tid; k < M; k += T) rU[k] = 1.0 / LU[k * M + k];
     if (tid == 0) *nb_out = nb;
+}
+
+// Partial-pivoting dense LU of one M x M row-major matrix, in place, by one
+// CTA: the pivoted fallback of columnsolve.factor_with_fallback
+// (columnsolve.py:141-153; scipy.linalg.lu_factor = LAPACK getrf semantics:
+// piv[k] = row interchanged with row k, first max |a_ik| wins, an exactly
+// zero pivot is reported through *info = k+1 and its column is not scaled).
+__device__ void lu_pivot_cta(double* LU, int* piv, int M, int* info) {
+    __shared__ double rv[256];
+    __shared__ int ri[256];
+    __shared__ int s_p;
+    const int tid = threadIdx.x, T = blockDim.x;
+    if (tid == 0 && info) *info = 0;
+    for (int k = 0; k < M; ++k) {
+        double best = -1.0;
+        int bi = M;
+        for (int r = k + tid; r < M; r += T) {
+            const double v = fabs(LU[r * M + k]);
+            if (v > best || (v == best && r < bi)) { best = v; bi = r; }
+        }
+        rv[tid] = best;
+        ri[tid] = bi;
+        __syncthreads();
+        for (int s = T / 2; s > 0; s >>= 1) {
+            if (tid < s) {
+                const double v = rv[tid + s];
+                const int i = ri[tid + s];
+                if (v > rv[tid] || (v == rv[tid] && i < ri[tid])) { rv[tid] = v; ri[tid] = i; }
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            s_p = ri[0];
+            piv[k] = ri[0];
+            if (rv[0] == 0.0 && info && *info == 0) *info = k + 1;
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (p != k)
+            for (int c = tid; c < M; c += T) {
+                const double t = LU[k * M + c];
+                LU[k * M + c] = LU[p * M + c];
+                LU[p * M + c] = t;
+            }
+        __syncthreads();
+        const double pv = LU[k * M + k];
+        if (pv != 0.0)
+            for (int r = k + 1 + tid; r < M; r += T) LU[r * M + k] /= pv;
+        __syncthreads();
+        const int n = M - (k + 1);
+        for (int t = tid; t < n * n; t += T) {
+            const int r = k + 1 + t / n, c = k + 1 + t % n;
+            LU[r * M + c] -= LU[r * M + k] * LU[k * M + c];
+        }
+        __syncthreads();
+    }
+}
+
+// plan factor fallback: LUP = pivoted LU of the shared column matrix A
+__global__ void k_lu_pivot(const double* A, double* LUP, int* piv, int M, int* info) {
+    for (int i = threadIdx.x; i < M * M; i += blockDim.x) LUP[i] = A[i];
+    __syncthreads();
+    lu_pivot_cta(LUP, piv, M, info);
+}
+
+// batched API (columnsolve.factor_with_fallback): one CTA per column
+__global__ void k_lu_pivot_batched(double* A, int* piv, int M, int* info) {
+    const long long c = blockIdx.x;
+    lu_pivot_cta(A + c * M * M, piv + c * M, M, info + c);
+}
+
+// batched pivoted substitution (scipy.linalg.lu_solve): one thread per column
+__global__ void k_lu_pivot_solve(const double* LU, const int* piv, double* x, int n_col, int M) {
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_col) return;
+    const double* A = LU + c * M * M;
+    const int* pv = piv + c * M;
+    double* b = x + c * M;
+    for (int i = 0; i < M; ++i) {
+        const int p = pv[i];
+        if (p != i) {
+            const double t = b[i];
+            b[i] = b[p];
+            b[p] = t;
+        }
+    }
+    for (int i = 1; i < M; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < i; ++j) s = fma(A[i * M + j], b[j], s);
+        b[i] -= s;
+    }
+    for (int i = M - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int j = i + 1; j < M; ++j) s = fma(A[i * M + j], b[j], s);
+        b[i] = (b[i] - s) / A[i * M + i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Run diagnostics (bench.total_mass / max_perturbations, bench.py:131-137) on
+// the lattice: mass = sum_g Wx Wy Wz (rho0 + rho'), max |rho'|, max |q4|.
+// Fixed grid and reduction order, so the result is bitwise reproducible.
+// ---------------------------------------------------------------------------
+constexpr int DIAG_BLOCKS = 592, DIAG_T = 256;
+
+__global__ void k_diag_partial(Geo g, const double* __restrict__ q, const double* __restrict__ rho0,
+                               const double* __restrict__ wx, const double* __restrict__ wy,
+                               const double* __restrict__ wz, double* part) {
+    __shared__ double sm[3][DIAG_T];
+    const long long n = (long long)g.Z * g.lY * g.lX;
+    double m = 0.0, mr = 0.0, mt = 0.0;
+    for (long long i = (long long)blockIdx.x * DIAG_T + threadIdx.x; i < n;
+         i += (long long)DIAG_BLOCKS * DIAG_T) {
+        const int x = (int)(i % g.lX);
+        const long long t = i / g.lX;
+        const int y = (int)(t % g.lY);
+        const int z = (int)(t / g.lY);
+        const long long o = ((long long)z * g.lY + y) * g.px + x;
+        const double r = q[o], th = q[o + 4 * g.fs];
+        m = fma(wz[z] * wy[y + g.y0] * wx[x + g.x0], rho0[z] + r, m);
+        mr = fmax(mr, fabs(r));
+        mt = fmax(mt, fabs(th));
+    }
+    sm[0][threadIdx.x] = m;
+    sm[1][threadIdx.x] = mr;
+    sm[2][threadIdx.x] = mt;
+    __syncthreads();
+    for (int s = DIAG_T / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            sm[0][threadIdx.x] += sm[0][threadIdx.x + s];
+            sm[1][threadIdx.x] = fmax(sm[1][threadIdx.x], sm[1][threadIdx.x + s]);
+            sm[2][threadIdx.x] = fmax(sm[2][threadIdx.x], sm[2][threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sm[0][0];
+        part[DIAG_BLOCKS + blockIdx.x] = sm[1][0];
+        part[2 * DIAG_BLOCKS + blockIdx.x] = sm[2][0];
+    }
+}
+
+__global__ void k_diag_final(const double* part, double* out) {
+    if (threadIdx.x != 0) return;
+    double m = 0.0, mr = 0.0, mt = 0.0;
+    for (int b = 0; b < DIAG_BLOCKS; ++b) {
+        m += part[b];
+        mr = fmax(mr, part[DIAG_BLOCKS + b]);
+        mt = fmax(mt, part[2 * DIAG_BLOCKS + b]);
+    }
+    out[0] = m;
+    out[1] = mr;
+    out[2] = mt;
 }
 
 // ---------------------------------------------------------------------------
@@ -925,6 +1085,11 @@ struct Factor {
     double* LU2 = nullptr;     // M*(4N+1)
     double* rU = nullptr;      // M
     int* d_nb = nullptr;
+    unsigned* d_bad = nullptr; // degenerate no-pivot diagonal seen
+    int pivoted = 0;           // factor_with_fallback took the pivoted path
+    double* LUP = nullptr;     // M*M pivoted dense LU
+    int* piv = nullptr;        // M interchanges
+    int* d_info = nullptr;
 };
 
 struct hevi_plan {
@@ -939,6 +1104,7 @@ struct hevi_plan {
     std::map<long long, Factor> factors;
     double bc[16];
     int eqset = 0;   // 0: set2nc, 1: set2c
+    int force_pivoted = 0;   // HEVI_OPT_FORCE_PIVOTED (tests of the fallback path)
     unsigned long long* d_dbg = nullptr;
     bool use_v2 = true;
     bool use_v3 = false;
@@ -992,24 +1158,24 @@ int dispatch_e(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     const int N = pl->N, Ny = pl->Ny;
     if (Ny == N) {
         switch (N) {
-            case 1: return launch_e<1, 1, MODE>(pl, a, st);
-            case 2: return launch_e<2, 2, MODE>(pl, a, st);
-            case 3: return launch_e<3, 3, MODE>(pl, a, st);
-            case 4: return launch_e<4, 4, MODE>(pl, a, st);
-            case 5: return launch_e<5, 5, MODE>(pl, a, st);
-            case 6: return launch_e<6, 6, MODE>(pl, a, st);
-            case 7: return launch_e<7, 7, MODE>(pl, a, st);
-            case 8: return launch_e<8, 8, MODE>(pl, a, st);
+            case 1: return launch_e<DN(1), 1, MODE>(pl, a, st);
+            case 2: return launch_e<DN(2), DN(2), MODE>(pl, a, st);
+            case 3: return launch_e<DN(3), DN(3), MODE>(pl, a, st);
+            case 4: return launch_e<DN(4), DN(4), MODE>(pl, a, st);
+            case 5: return launch_e<DN(5), DN(5), MODE>(pl, a, st);
+            case 6: return launch_e<DN(6), DN(6), MODE>(pl, a, st);
+            case 7: return launch_e<DN(7), DN(7), MODE>(pl, a, st);
+            case 8: return launch_e<DN(8), DN(8), MODE>(pl, a, st);
         }
     } else if (Ny == 1) {
         switch (N) {
-            case 2: return launch_e<2, 1, MODE>(pl, a, st);
-            case 3: return launch_e<3, 1, MODE>(pl, a, st);
-            case 4: return launch_e<4, 1, MODE>(pl, a, st);
-            case 5: return launch_e<5, 1, MODE>(pl, a, st);
-            case 6: return launch_e<6, 1, MODE>(pl, a, st);
-            case 7: return launch_e<7, 1, MODE>(pl, a, st);
-            case 8: return launch_e<8, 1, MODE>(pl, a, st);
+            case 2: return launch_e<DN(2), 1, MODE>(pl, a, st);
+            case 3: return launch_e<DN(3), 1, MODE>(pl, a, st);
+            case 4: return launch_e<DN(4), 1, MODE>(pl, a, st);
+            case 5: return launch_e<DN(5), 1, MODE>(pl, a, st);
+            case 6: return launch_e<DN(6), 1, MODE>(pl, a, st);
+            case 7: return launch_e<DN(7), 1, MODE>(pl, a, st);
+            case 8: return launch_e<DN(8), 1, MODE>(pl, a, st);
         }
     }
     return fail("unsupported polynomial order (supported: N = 1..8; slab Ny = 1)");
@@ -1125,7 +1291,7 @@ int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) 
             attr = smem;
         }
         CUtensorMap tm;
-        int rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, T::NL);
+        int rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, 1);   // one level per TMA
         if (rc) return rc;
         dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
         kern<<<grid, T::BLK, smem, st>>>(a, tm);
@@ -1141,23 +1307,23 @@ int dispatch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done
     done = false;
     if (Ny == N) {
         switch (N) {
-            case 1: return launch_e2<1, 1, MODE>(pl, a, st, done);
-            case 2: return launch_e2<2, 2, MODE>(pl, a, st, done);
-            case 3: return launch_e2<3, 3, MODE>(pl, a, st, done);
-            case 4: return launch_e2<4, 4, MODE>(pl, a, st, done);
-            case 5: return launch_e2<5, 5, MODE>(pl, a, st, done);
-            case 6: return launch_e2<6, 6, MODE>(pl, a, st, done);
-            case 7: return launch_e2<7, 7, MODE>(pl, a, st, done);
+            case 1: return launch_e2<DN(1), 1, MODE>(pl, a, st, done);
+            case 2: return launch_e2<DN(2), DN(2), MODE>(pl, a, st, done);
+            case 3: return launch_e2<DN(3), DN(3), MODE>(pl, a, st, done);
+            case 4: return launch_e2<DN(4), DN(4), MODE>(pl, a, st, done);
+            case 5: return launch_e2<DN(5), DN(5), MODE>(pl, a, st, done);
+            case 6: return launch_e2<DN(6), DN(6), MODE>(pl, a, st, done);
+            case 7: return launch_e2<DN(7), DN(7), MODE>(pl, a, st, done);
         }
     } else if (Ny == 1) {
         switch (N) {
-            case 2: return launch_e2<2, 1, MODE>(pl, a, st, done);
-            case 3: return launch_e2<3, 1, MODE>(pl, a, st, done);
-            case 4: return launch_e2<4, 1, MODE>(pl, a, st, done);
-            case 5: return launch_e2<5, 1, MODE>(pl, a, st, done);
-            case 6: return launch_e2<6, 1, MODE>(pl, a, st, done);
-            case 7: return launch_e2<7, 1, MODE>(pl, a, st, done);
-            case 8: return launch_e2<8, 1, MODE>(pl, a, st, done);
+            case 2: return launch_e2<DN(2), 1, MODE>(pl, a, st, done);
+            case 3: return launch_e2<DN(3), 1, MODE>(pl, a, st, done);
+            case 4: return launch_e2<DN(4), 1, MODE>(pl, a, st, done);
+            case 5: return launch_e2<DN(5), 1, MODE>(pl, a, st, done);
+            case 6: return launch_e2<DN(6), 1, MODE>(pl, a, st, done);
+            case 7: return launch_e2<DN(7), 1, MODE>(pl, a, st, done);
+            case 8: return launch_e2<DN(8), 1, MODE>(pl, a, st, done);
         }
     }
     return HEVI_OK;
@@ -1220,22 +1386,22 @@ int dispatch_c(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     const int N = pl->N, Ny = pl->Ny;
     if (Ny == N) {
         switch (N) {
-            case 1: return launch_c<1, 1, MODE>(pl, a, st);
-            case 2: return launch_c<2, 2, MODE>(pl, a, st);
-            case 3: return launch_c<3, 3, MODE>(pl, a, st);
-            case 4: return launch_c<4, 4, MODE>(pl, a, st);
-            case 5: return launch_c<5, 5, MODE>(pl, a, st);
-            case 6: return launch_c<6, 6, MODE>(pl, a, st);
+            case 1: return launch_c<DN(1), 1, MODE>(pl, a, st);
+            case 2: return launch_c<DN(2), DN(2), MODE>(pl, a, st);
+            case 3: return launch_c<DN(3), DN(3), MODE>(pl, a, st);
+            case 4: return launch_c<DN(4), DN(4), MODE>(pl, a, st);
+            case 5: return launch_c<DN(5), DN(5), MODE>(pl, a, st);
+            case 6: return launch_c<DN(6), DN(6), MODE>(pl, a, st);
         }
     } else if (Ny == 1) {
         switch (N) {
-            case 2: return launch_c<2, 1, MODE>(pl, a, st);
-            case 3: return launch_c<3, 1, MODE>(pl, a, st);
-            case 4: return launch_c<4, 1, MODE>(pl, a, st);
-            case 5: return launch_c<5, 1, MODE>(pl, a, st);
-            case 6: return launch_c<6, 1, MODE>(pl, a, st);
-            case 7: return launch_c<7, 1, MODE>(pl, a, st);
-            case 8: return launch_c<8, 1, MODE>(pl, a, st);
+            case 2: return launch_c<DN(2), 1, MODE>(pl, a, st);
+            case 3: return launch_c<DN(3), 1, MODE>(pl, a, st);
+            case 4: return launch_c<DN(4), 1, MODE>(pl, a, st);
+            case 5: return launch_c<DN(5), 1, MODE>(pl, a, st);
+            case 6: return launch_c<DN(6), 1, MODE>(pl, a, st);
+            case 7: return launch_c<DN(7), 1, MODE>(pl, a, st);
+            case 8: return launch_c<DN(8), 1, MODE>(pl, a, st);
         }
     }
     return fail("set2c: unsupported polynomial order for the device path");
@@ -1338,6 +1504,20 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
     a.out = a1.out;
     a.src_uv = a1.src_uv;
     const int T = 128;
+    if (f->pivoted) {   // columnsolve.factor_with_fallback: pivoted dense factor
+        a.LU2 = f->LUP;
+        const size_t smp = sizeof(double) * ((size_t)V_NT * M + (size_t)M * M + (N + 1) * (N + 1) +
+                                             (size_t)M * T) + sizeof(int) * M;
+        if (smp > 225 * 1024) return fail("column too tall for the pivoted column kernel");
+        auto kern = pl->eqset == 1 ? k_solve_piv<N, true> : k_solve_piv<N, false>;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+        const int NYp = g.slab ? 1 : pl->N;
+        const long long nc = ((long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0)) *
+                             ((long long)(g.ey_e - g.ey_b) * NYp + (g.ey_e == g.ney ? 1 : 0));
+        kern<<<(int)((nc + T - 1) / T), T, smp, st>>>(a, f->piv);
+        CK(cudaGetLastError());
+        return HEVI_OK;
+    }
     const size_t smem = sizeof(double) * ((size_t)V_NT * M + (size_t)M * (4 * N + 1) + M +
                                           (N + 1) * (N + 1) + (size_t)M * T);
     if (smem > 225 * 1024) return fail("column too tall for the v2 column kernel");
@@ -1368,20 +1548,20 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
 
 int run_s2(const hevi_plan* pl, const Factor* f, const SArgs& a, cudaStream_t st, bool& done) {
     done = false;
-    if (!pl->use_v2 || f->nb > 2 * pl->N + 1) return HEVI_OK;
+    if (!pl->use_v2 || (f->nb > 2 * pl->N + 1 && !f->pivoted)) return HEVI_OK;
     const size_t need = sizeof(double) * ((size_t)V_NT * pl->g.Z +
                                           (size_t)pl->g.Z * (4 * pl->N + 1 + 1 + 128));
     if (need > 220 * 1024) return HEVI_OK;
     int rc = HEVI_OK;
     switch (pl->N) {
-        case 1: rc = launch_s2<1>(pl, f, a, st); break;
-        case 2: rc = launch_s2<2>(pl, f, a, st); break;
-        case 3: rc = launch_s2<3>(pl, f, a, st); break;
-        case 4: rc = launch_s2<4>(pl, f, a, st); break;
-        case 5: rc = launch_s2<5>(pl, f, a, st); break;
-        case 6: rc = launch_s2<6>(pl, f, a, st); break;
-        case 7: rc = launch_s2<7>(pl, f, a, st); break;
-        case 8: rc = launch_s2<8>(pl, f, a, st); break;
+        case 1: rc = launch_s2<DN(1)>(pl, f, a, st); break;
+        case 2: rc = launch_s2<DN(2)>(pl, f, a, st); break;
+        case 3: rc = launch_s2<DN(3)>(pl, f, a, st); break;
+        case 4: rc = launch_s2<DN(4)>(pl, f, a, st); break;
+        case 5: rc = launch_s2<DN(5)>(pl, f, a, st); break;
+        case 6: rc = launch_s2<DN(6)>(pl, f, a, st); break;
+        case 7: rc = launch_s2<DN(7)>(pl, f, a, st); break;
+        case 8: rc = launch_s2<DN(8)>(pl, f, a, st); break;
         default: return HEVI_OK;
     }
     done = (rc == HEVI_OK);
@@ -1403,17 +1583,18 @@ int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st) {
         if (f) {
             int rc = run_s2(pl, f, a, st, done);
             if (rc || done) return rc;
+            if (f->pivoted) return fail("pivoted column factor needs the v2 column kernel");
         }
     }
     switch (pl->N) {
-        case 1: return launch_s<1>(pl, a, st);
-        case 2: return launch_s<2>(pl, a, st);
-        case 3: return launch_s<3>(pl, a, st);
-        case 4: return launch_s<4>(pl, a, st);
-        case 5: return launch_s<5>(pl, a, st);
-        case 6: return launch_s<6>(pl, a, st);
-        case 7: return launch_s<7>(pl, a, st);
-        case 8: return launch_s<8>(pl, a, st);
+        case 1: return launch_s<DN(1)>(pl, a, st);
+        case 2: return launch_s<DN(2)>(pl, a, st);
+        case 3: return launch_s<DN(3)>(pl, a, st);
+        case 4: return launch_s<DN(4)>(pl, a, st);
+        case 5: return launch_s<DN(5)>(pl, a, st);
+        case 6: return launch_s<DN(6)>(pl, a, st);
+        case 7: return launch_s<DN(7)>(pl, a, st);
+        case 8: return launch_s<DN(8)>(pl, a, st);
     }
     return fail("unsupported polynomial order");
 }
@@ -1575,6 +1756,10 @@ int hevi_plan_destroy(hevi_plan* pl) {
         cudaFree(kv.second.LU2);
         cudaFree(kv.second.rU);
         cudaFree(kv.second.d_nb);
+        cudaFree(kv.second.d_bad);
+        cudaFree(kv.second.LUP);
+        cudaFree(kv.second.piv);
+        cudaFree(kv.second.d_info);
     }
     cudaFree(pl->d_tab);
     cudaFree(pl->d_flags);
@@ -1603,6 +1788,8 @@ int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
         CK(cudaMalloc(&f.LU2, sizeof(double) * M * (4 * pl->N + 1)));
         CK(cudaMalloc(&f.rU, sizeof(double) * M));
         CK(cudaMalloc(&f.d_nb, sizeof(int)));
+        CK(cudaMalloc(&f.d_bad, sizeof(unsigned)));
+        CK(cudaMemsetAsync(f.d_bad, 0, sizeof(unsigned), st));
         CK(cudaMemsetAsync(f.A, 0, sizeof(double) * M * M, st));
         FArgs a;
         a.lv = pl->lv;
@@ -1623,11 +1810,22 @@ int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
         CK(cudaGetLastError());
         k_probe<<<(M + 63) / 64, 64, 0, st>>>(a);
         CK(cudaGetLastError());
-        k_lu_dense<<<1, 256, 0, st>>>(f.A, f.LU, f.LUb, M, f.d_nb, pl->d_flags, pl->N, f.LU2,
-                                      f.rU);
+        k_lu_dense<<<1, 256, 0, st>>>(f.A, f.LU, f.LUb, M, f.d_nb, f.d_bad, pl->N, f.LU2, f.rU);
         CK(cudaGetLastError());
+        unsigned bad = 0;
         CK(cudaMemcpyAsync(&f.nb, f.d_nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&bad, f.d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (bad || pl->force_pivoted) {
+            // columnsolve.factor_with_fallback (:141-153): keep a pivoted dense LU
+            CK(cudaMalloc(&f.LUP, sizeof(double) * M * M));
+            CK(cudaMalloc(&f.piv, sizeof(int) * M));
+            CK(cudaMalloc(&f.d_info, sizeof(int)));
+            k_lu_pivot<<<1, 256, 0, st>>>(f.A, f.LUP, f.piv, M, f.d_info);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(st));
+            f.pivoted = 1;
+        }
         it = pl->factors.emplace(lam_key(lam), f).first;
     }
     if (nb_out) *nb_out = it->second.nb;
@@ -1859,6 +2057,61 @@ int hevi_band_solve(const double* band, double* rhs, int n_col, int M, int nb, v
     if (!band || !rhs || n_col < 1 || M < 1 || nb < 1) return fail("bad band_solve arguments");
     k_band_solve<<<(n_col + 127) / 128, 128, 0, (cudaStream_t)stream>>>(band, rhs, n_col, M, nb);
     CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_plan_set_option(hevi_plan* pl, int option, int value) {
+    if (!pl) return fail("null plan");
+    if (option == HEVI_OPT_FORCE_PIVOTED) {
+        pl->force_pivoted = value != 0;
+        return HEVI_OK;
+    }
+    return fail("unknown plan option");
+}
+
+int hevi_factor_pivoted(const hevi_plan* pl, double lam, int* pivoted) {
+    const Factor* f = pl ? find_factor(pl, lam) : nullptr;
+    if (!f) {
+        g_err = "lam not factored";
+        return HEVI_ENOFACTOR;
+    }
+    if (pivoted) *pivoted = f->pivoted;
+    return HEVI_OK;
+}
+
+int hevi_lu_pivot(double* A, int* piv, int n_col, int M, int* info_host, void* stream) {
+    if (!A || !piv || n_col < 1 || M < 1) return fail("bad lu_pivot arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    int* d_info;
+    CK(cudaMallocAsync(&d_info, sizeof(int) * n_col, st));
+    k_lu_pivot_batched<<<n_col, 256, 0, st>>>(A, piv, M, d_info);
+    CK(cudaGetLastError());
+    if (info_host) CK(cudaMemcpyAsync(info_host, d_info, sizeof(int) * n_col, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d_info, st));
+    CK(cudaStreamSynchronize(st));
+    return HEVI_OK;
+}
+
+int hevi_lu_pivot_solve(const double* LU, const int* piv, double* rhs, int n_col, int M, void* stream) {
+    if (!LU || !piv || !rhs || n_col < 1 || M < 1) return fail("bad lu_pivot_solve arguments");
+    k_lu_pivot_solve<<<(n_col + 127) / 128, 128, 0, (cudaStream_t)stream>>>(LU, piv, rhs, n_col, M);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_diagnostics(const hevi_plan* pl, const double* q, const double* wx, const double* wy,
+                     const double* wz, double* out_host, void* stream) {
+    if (!pl || !q || !wx || !wy || !wz || !out_host) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    double* d;
+    CK(cudaMallocAsync(&d, sizeof(double) * (3 * DIAG_BLOCKS + 3), st));
+    k_diag_partial<<<DIAG_BLOCKS, DIAG_T, 0, st>>>(pl->g, q, pl->lv.rho0, wx, wy, wz, d);
+    CK(cudaGetLastError());
+    k_diag_final<<<1, 32, 0, st>>>(d, d + 3 * DIAG_BLOCKS);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_host, d + 3 * DIAG_BLOCKS, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d, st));
+    CK(cudaStreamSynchronize(st));
     return HEVI_OK;
 }
 

@@ -238,3 +238,141 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     }
 #undef TB
 }
+
+// ---------------------------------------------------------------------------
+// Pivoted fallback of the fused column solve (columnsolve.py:141-167): the
+// shared column matrix carries a partial-pivoting dense LU (k_lu_pivot) when
+// the no-pivot banded LU hits a degenerate diagonal.  One thread per column:
+// Schur RHS of every level into shared memory, row interchanges, dense L and
+// U substitution (scipy.linalg.lu_solve), then the same extraction as
+// k_solve2.  Arguments as S2Args with LU2 = the M x M pivoted factor and
+// piv its interchanges.
+// ---------------------------------------------------------------------------
+template <int N, bool SC>
+__global__ void __launch_bounds__(128) k_solve_piv(const S2Args a, const int* __restrict__ piv) {
+    extern __shared__ __align__(16) double smp[];
+    const Geo& g = a.g;
+    const int M = g.Z;
+    const int T = blockDim.x;
+    const int tid = threadIdx.x;
+    double* tb = smp;                   // V_NT * M
+    double* LU = tb + V_NT * M;         // M * M
+    double* sD = LU + M * M;            // (N+1)^2
+    double* Y = sD + (N + 1) * (N + 1); // M * T
+    int* sp = reinterpret_cast<int*>(Y + (size_t)M * T);   // M
+    for (int i = tid; i < V_NT * M; i += T) tb[i] = a.tab[i];
+    for (int i = tid; i < M * M; i += T) LU[i] = a.LU2[i];
+    for (int i = tid; i < (N + 1) * (N + 1); i += T) sD[i] = a.Dz[i];
+    for (int i = tid; i < M; i += T) sp[i] = piv[i];
+    __syncthreads();
+
+    const int NYo = g.slab ? 1 : N;
+    const int xlo = g.ex_b * N;
+    const int cntx = (g.ex_e - g.ex_b) * N + (g.ex_e == g.nex ? 1 : 0);
+    const int ylo = g.ey_b * NYo;
+    const int cnty = (g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
+    const int c = blockIdx.x * T + tid;
+    if (c >= cntx * cnty) return;
+    const int gx = xlo + c % cntx;
+    const int gy = ylo + c / cntx;
+    const int gys = g.slab ? 0 : gy;
+    const long long fs = g.fs;
+    const double lam = a.lam, gr = a.ph.g;
+    const bool ident = a.ainv_identity != 0;
+    const int nez = g.nez;
+    const double* Ps = a.P + loff(g, gx, gys, 0);
+    const double* Po = a.P + loff(g, gx, gy, 0);
+    double* Oo = a.out + loff(g, gx, gy, 0);
+    const long long ls = (long long)g.lY * g.px;
+#define TB(t, k) tb[(t) * M + (k)]
+#define YY(k) Y[(size_t)(k) * T + tid]
+    auto ua_at = [&](int k, const double* src) -> double {
+        const long long o = (long long)k * ls;
+        const double re = src[o], we = src[o + 3 * fs], te = src[o + 4 * fs];
+        double v = SC ? we - (lam * (re - te * TB(V_ITH0, k))) * gr : we + (TB(V_COEF, k) * te) * gr;
+        if (!ident) v = v - TB(V_UA, k) * ((TB(V_DTH0, k) * v) / TB(V_DEN, k));
+        return (k == 0 || k == M - 1) ? 0.0 : v;
+    };
+    // folded z-derivative at level k of a per-level quantity f(k') (DSS across element faces)
+    auto dz_at = [&](int k, auto&& f) -> double {
+        const int e = (k == M - 1) ? nez - 1 : k / N;
+        const int l = k - e * N;
+        double d = 0.0;
+        for (int m = 0; m <= N; ++m) d = fma(sD[l * (N + 1) + m], f(e * N + m), d);
+        if (l == 0 && e > 0) {
+            double d2 = 0.0;
+            for (int m = 0; m <= N; ++m) d2 = fma(sD[N * (N + 1) + m], f((e - 1) * N + m), d2);
+            d += d2;
+        }
+        return d;
+    };
+    // 1. Schur RHS (imexcore.py:229-243, _helmholtz_flux :259-268) of every level
+    for (int k = 0; k < M; ++k) {
+        const long long o = (long long)k * ls;
+        const double re = Ps[o], te = Ps[o + 4 * fs];
+        const double ua = ua_at(k, Ps);
+        const double dua = TB(V_CZ, k) * dz_at(k, [&](int kk) { return ua_at(kk, Ps); });
+        const double Pe = SC ? TB(V_F0C, k) * te : TB(V_G0, k) * re + TB(V_H0, k) * te;
+        YY(k) = SC ? Pe - TB(V_F0C, k) * lam * (TB(V_TH0, k) * dua + TB(V_DTH0, k) * ua)
+                   : Pe - lam * (TB(V_F0Z, k) * ua + TB(V_RG, k) * dua);
+    }
+    // 2. interchanges, unit-lower and upper substitution
+    for (int i = 0; i < M; ++i) {
+        const int p = sp[i];
+        if (p != i) {
+            const double t = YY(i);
+            YY(i) = YY(p);
+            YY(p) = t;
+        }
+    }
+    for (int i = 1; i < M; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < i; ++j) s = fma(LU[i * M + j], YY(j), s);
+        YY(i) = YY(i) - s;
+    }
+    for (int i = M - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int j = i + 1; j < M; ++j) s = fma(LU[i * M + j], YY(j), s);
+        YY(i) = (YY(i) - s) / LU[i * M + i];
+    }
+    // 3. extraction of w, theta', rho' (imexcore.py:245-298), as k_solve2
+    for (int k = 0; k < M; ++k) {
+        const long long o = (long long)k * ls;
+        const double re = Po[o], we = Po[o + 3 * fs], te = Po[o + 4 * fs];
+        const double Pk = YY(k);
+        const bool bz = (k == 0) || (k == M - 1);
+        const double dP = TB(V_CZ, k) * dz_at(k, [&](int kk) { return YY(kk); });
+        double up = SC ? lam * (dP + (Pk * TB(V_IFT, k)) * gr)
+                       : lam * (dP * TB(V_IRHO0, k) + (Pk * TB(V_IG0R, k)) * gr);
+        double ua = SC ? we - (lam * (re - te * TB(V_ITH0, k))) * gr : we + (TB(V_COEF, k) * te) * gr;
+        if (!ident) {
+            ua = ua - TB(V_UA, k) * ((TB(V_DTH0, k) * ua) / TB(V_DEN, k));
+            up = up - TB(V_UA, k) * ((TB(V_DTH0, k) * up) / TB(V_DEN, k));
+        }
+        if (bz) {
+            ua = 0.0;
+            up = 0.0;
+        }
+        const double w = ua - up;
+        double th, rho;
+        if (SC) {
+            th = Pk / TB(V_F0C, k);
+            rho = ((Pk * TB(V_IFT, k) + (lam * TB(V_ITH0, k)) * (w * TB(V_DTH0, k))) - te * TB(V_ITH0, k)) + re;
+        } else {
+            th = te - lam * (w * TB(V_DTH0, k));
+            rho = (Pk - TB(V_H0, k) * th) * TB(V_IG0, k);
+        }
+        Oo[o] = rho;
+        Oo[o + 3 * fs] = w;
+        Oo[o + 4 * fs] = th;
+        if (a.src_uv) {
+            const bool bx = (gx == 0) || (gx == g.X - 1);
+            const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
+            const double* su = a.src_uv + loff(g, gx, gy, k);
+            Oo[o + fs] = bx ? 0.0 : su[fs];
+            Oo[o + 2 * fs] = by ? 0.0 : su[2 * fs];
+        }
+    }
+#undef YY
+#undef TB
+}

@@ -242,3 +242,34 @@ def _generic_step(q, dt, tableau, problem, rhs):
     if not finite:
         raise FloatingPointError("non-finite state after IMEX step")
     return out
+
+
+@dataclass
+class BdfCoefficients:
+    """imexcore.py:66-70."""
+    alpha: np.ndarray
+    beta: np.ndarray
+    chi: float
+
+
+def bdf2_coefficients() -> BdfCoefficients:
+    """imexcore.py:73-76."""
+    return BdfCoefficients(alpha=np.array([4.0 / 3.0, -1.0 / 3.0]),
+                           beta=np.array([2.0, -1.0]), chi=2.0 / 3.0)
+
+
+def bdf2_imex_step(qn, qnm1, dt: float, coeffs: BdfCoefficients, problem, rhs):
+    """Two-step BDF2 IMEX step (imexcore.py:417-430): two R evaluations and one
+    implicit solve with lam = chi dt, all on the device; the combinations are
+    elementwise on the device E-vectors."""
+    al, be, chi = coeffs.alpha, coeffs.beta, coeffs.chi
+    problem.lam = chi * dt
+    qe = (al[0] * qn + al[1] * qnm1
+          + chi * dt * (be[0] * rhs(qn) + be[1] * rhs(qnm1)))
+    shift = be[0] * qn + be[1] * qnm1
+    qtt = problem.solve(qe - shift)
+    out = qtt + shift
+    finite = np.isfinite(out).all() if isinstance(out, np.ndarray) else bool(out.isfinite().all())
+    if not finite:
+        raise FloatingPointError("non-finite state after IMEX step")
+    return out

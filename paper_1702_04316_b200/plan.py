@@ -134,6 +134,17 @@ class HeviPlan:
         nv.check(self.lib.hevi_factor(self.h, float(lam), ctypes.byref(nb), nv.stream_ptr()))
         return nb.value
 
+    def force_pivoted(self, on=True):
+        """Keep the pivoted dense column factor for lam values factored from
+        now on (HEVI_OPT_FORCE_PIVOTED: exercises factor_with_fallback)."""
+        nv.check(self.lib.hevi_plan_set_option(self.h, 1, int(bool(on))))
+
+    def factor_pivoted(self, lam) -> bool:
+        """Whether the factor of lam took the pivoted fallback."""
+        p = ctypes.c_int(0)
+        nv.check(self.lib.hevi_factor_pivoted(self.h, float(lam), ctypes.byref(p)))
+        return bool(p.value)
+
     def column_matrix(self, lam):
         M = self.Z
         self.factor(lam)

@@ -1,0 +1,54 @@
+"""Device simulation driver against the unmodified reference driver
+(cli.run_simulation) on its 2D slab bubble / rest state: step counts, dt,
+solve counts, the time-series CSV (mass, max |rho'|, max |theta'|, probe)
+and the final snapshot table (goldens: tests/golden/make_driver_golden.py)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from paper_1702_04316_b200 import driver  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def load(name):
+    return np.load(os.path.join(HERE, "golden", f"driver_{name}.npz"))
+
+
+@pytest.mark.parametrize("name", ["ark2", "rk35", "bdf2_c", "ark2_rest"])
+def test_run_matches_reference_driver(name, tmp_path):
+    g = load(name)
+    cfg = driver.parse_config(None, list(g["overrides"]) + [f"--output_dir={tmp_path}"])
+    res = driver.run_simulation(cfg, quiet=True)
+    assert res.exit_code == int(g["exit_code"]) == 0
+    assert res.steps == int(g["steps"])
+    assert res.dt == pytest.approx(float(g["dt"]), rel=1e-13)
+    assert res.stats.solves == int(g["solves"])
+    ts = np.genfromtxt(tmp_path / "timeseries.csv", delimiter=",", names=True)
+    mine = np.array([list(r) for r in ts])
+    want = g["ts"]
+    assert mine.shape == want.shape
+    assert open(tmp_path / "timeseries.csv").readline() == str(g["csv"]).splitlines()[0] + "\n"
+    np.testing.assert_allclose(mine[:, 0], want[:, 0], rtol=1e-13)            # time
+    np.testing.assert_allclose(mine[:, 1], want[:, 1], rtol=1e-13)            # mass
+    # max |rho'|, max |theta'|, probe P': relative 1e-8 with absolute floors for
+    # states that are round-off noise in the reference (rest state)
+    floor = np.array([1e-6, 1e-4, 1e-2])     # P' floor: ulp(P0) ~ 1.5e-11 Pa
+    scale = np.maximum(np.abs(want[:, 2:]).max(axis=0), floor)
+    assert (np.abs(mine[:, 2:] - want[:, 2:]).max(axis=0) <= 1e-8 * scale).all()
+    snaps = [f for f in os.listdir(tmp_path) if f.startswith("snapshot_")]
+    assert snaps == [str(g["snapshot_name"])]
+    snap = np.loadtxt(tmp_path / snaps[0])
+    ref = g["snapshot"]
+    assert snap.shape == ref.shape
+    np.testing.assert_allclose(snap[:, :3], ref[:, :3], rtol=1e-9, atol=1e-9)   # coords
+    # rho_p, (u v w) as a vector (v in the slab is reference round-off), theta_p;
+    # 10 significant digits in the file
+    for cols, fl in (((3,), 1e-6), ((4, 5, 6), 1e-4), ((7,), 1e-4)):
+        s = max(np.abs(ref[:, list(cols)]).max(), fl)
+        err = np.abs(snap[:, list(cols)] - ref[:, list(cols)]).max()
+        assert err <= 1e-8 * s, (cols, err, s)

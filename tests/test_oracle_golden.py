@@ -65,3 +65,18 @@ def test_oracle_rk35_matches_reference():
         if k in (1, 10):
             errs = rel_fields(o.to_lattice(q), g[f"step_q{k}"])
             assert max(errs) < STEP_TOL, (k, errs)
+
+
+def test_oracle_pivoted_fallback_matches_banded():
+    """factor_with_fallback's pivoted path (columnsolve.py:141-167) gives the
+    banded trajectory: the Schur columns need no interchanges."""
+    name = "box3d_n4"
+    g = load_golden(name)
+    o, op = oracle_for(name), oracle_for(name)
+    op.force_pivoted = True
+    q = qp = o.from_lattice(g["step_q0"])
+    dt = float(g["step_dt"])
+    for _ in range(3):
+        q, qp = o.step(q, dt), op.step(qp, dt)
+    assert isinstance(op.factors(0.3, True)[0], str)
+    assert max(rel_fields(o.to_lattice(qp), o.to_lattice(q))) < 1e-12
