@@ -127,6 +127,29 @@ int hevi_flags(hevi_plan *plan, unsigned *flags, int reset, void *stream);
  *                  *bad_col receives the first degenerate column or -1
  * hevi_band_solve: columnsolve.solve_columns_direct (:156-181), rhs (n_col, M)
  *                  row-major, solved in place                                  */
+/* 3D-IMEX pressure (Schur) form, dim = "3d" (imexcore.py:200-298), and the
+ * full linear operator (euler.linear_operator, vertical_only=False,
+ * euler.py:313-365), on lattice arrays of this plan (vectors of 3 fields:
+ * ua, up, vel; field stride = the plan's):
+ *   hevi_linear3         out = L(q), 5 fields
+ *   hevi_schur3_up       up = ImplicitProblem._up(P)                (:245-257)
+ *   hevi_schur3_flux     out = P - _helmholtz_flux(vel)             (:259-268)
+ *                        (lhs_schur with vel = up; the Schur rhs with P = Pe, vel = ua)
+ *   hevi_schur3_ua       ua, Pe of rhs_schur_build                  (:229-243)
+ *   hevi_schur3_extract  q = extract_from_pressure(P, ua, q_e), up = _up(P)  (:273-298)
+ * Krylov vector kernels (krylov.py): hevi_wdot = the E-vector dot product of
+ * two continuous lattice fields (multiplicity-weighted, deterministic order);
+ * hevi_axpby: y = alpha x + beta y over n doubles. */
+int hevi_linear3(hevi_plan *plan, const double *q, double *out, void *stream);
+int hevi_schur3_up(hevi_plan *plan, double lam, const double *P, double *up, void *stream);
+int hevi_schur3_flux(hevi_plan *plan, double lam, const double *P, const double *vel, double *out,
+                     void *stream);
+int hevi_schur3_ua(hevi_plan *plan, double lam, const double *qe, double *ua, double *Pe, void *stream);
+int hevi_schur3_extract(hevi_plan *plan, double lam, const double *P, const double *ua,
+                        const double *up, const double *qe, double *q, void *stream);
+int hevi_wdot(const hevi_plan *plan, const double *x, const double *y, double *out_host, void *stream);
+int hevi_axpby(long long n, double alpha, const double *x, double beta, double *y, void *stream);
+
 /* Run diagnostics (bench.total_mass / max_perturbations, bench.py:131-137) of a
  * lattice state of this plan: out_host[0] = sum_g Wx[gx] Wy[gy] Wz[gz] (rho0 +
  * rho'), out_host[1] = max |rho'|, out_host[2] = max |q4|; Wx/Wy/Wz are the

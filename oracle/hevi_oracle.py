@@ -485,6 +485,72 @@ class BoxOracle:
         """imexcore.lhs_schur (imexcore.py:270-271)."""
         return P - self.helm(self.up(P, lam), lam)
 
+    # -- 3D-IMEX pieces, dim='3d' (euler.py:281-290, 313-365; imexcore.py:229-271)
+    def gradc(self, f):
+        """Discretization.gradc: DSS of every gradient component (euler.py:281-286)."""
+        g = self.grad(f)
+        return np.stack([self.dss(np.ascontiguousarray(g[..., m])) for m in range(3)], axis=-1)
+
+    def divc(self, vec):
+        """Discretization.divc (euler.py:288-290)."""
+        return self.dss(self.div(vec))
+
+    def linear3(self, q):
+        """euler.linear_operator, vertical_only=False, cG (euler.py:313-365)."""
+        vel = np.moveaxis(q[1:4], 0, -1)
+        if self.set_name == "set2c":
+            P = self.F0c * q[4]
+        else:
+            P = self.G0 * q[0] + self.H0 * q[4]
+        gradP = self.gradc(P)
+        divU = self.divc(vel)
+        out = np.zeros_like(q)
+        if self.set_name == "set2c":
+            out[0] = -divU
+            mom = -(gradP + q[0][..., None] * self.gvec)
+            out[4] = -(self.theta0 * divU + np.einsum("...a,...a->...", vel, self.grad_theta0))
+        else:
+            out[0] = -(np.einsum("...a,...a->...", vel, self.grad_rho0) + self.rho0 * divU)
+            mom = -(gradP / self.rho0[..., None] + (q[0] / self.rho0)[..., None] * self.gvec)
+            out[4] = -np.einsum("...a,...a->...", vel, self.grad_theta0)
+        out[1:4] = self.no_flux(np.moveaxis(mom, -1, 0))
+        return out
+
+    def helm3(self, vel, lam):
+        """imexcore._helmholtz_flux with divc (imexcore.py:259-268)."""
+        if self.set_name == "set2c":
+            return self.F0c * lam * (self.theta0 * self.divc(vel)
+                                     + np.einsum("...a,...a->...", self.grad_theta0, vel))
+        return lam * (np.einsum("...a,...a->...", self.F0vec, vel)
+                      + self.rho0 * self.G0 * self.divc(vel))
+
+    def up3(self, P, lam):
+        """imexcore._up with gradc (imexcore.py:245-257)."""
+        gP = self.gradc(P)
+        if self.set_name == "set2c":
+            v = self.ainv(lam * (gP + (P / (self.F0c * self.theta0))[..., None] * self.gvec), lam)
+        else:
+            v = self.ainv(lam * (gP / self.rho0[..., None]
+                                 + (P / (self.G0 * self.rho0))[..., None] * self.gvec), lam)
+        return self._nf(v)
+
+    def schur_rhs3(self, qe, lam):
+        """rhs_schur_build, dim='3d' (imexcore.py:229-243)."""
+        vel = np.moveaxis(qe[1:4], 0, -1)
+        if self.set_name == "set2c":
+            Pe = self.F0c * qe[4]
+            ua = self._nf(self.ainv(vel - (lam * (qe[0] - qe[4] / self.theta0))[..., None]
+                                    * self.gvec, lam))
+        else:
+            Pe = self.G0 * qe[0] + self.H0 * qe[4]
+            coef = lam * self.H0 / (self.G0 * self.rho0)
+            ua = self._nf(self.ainv(vel + (coef * qe[4])[..., None] * self.gvec, lam))
+        return Pe - self.helm3(ua, lam), ua
+
+    def lhs_schur3(self, P, lam):
+        """lhs_schur, dim='3d' (imexcore.py:270-271)."""
+        return P - self.helm3(self.up3(P, lam), lam)
+
     def extract(self, P, ua, qe, lam):
         """imexcore.extract_from_pressure set2nc, 1d (imexcore.py:273-287)."""
         vel = ua - self.up(P, lam)

@@ -1068,6 +1068,7 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 #include "explicit_v3.cuh"
 #include "explicit_c.cuh"
 #include "solve_v2.cuh"
+#include "imex3d.cuh"
 
 }  // namespace
 
@@ -2056,6 +2057,92 @@ int hevi_band_lu(double* band, int n_col, int M, int nb, double norm, int* bad_c
 int hevi_band_solve(const double* band, double* rhs, int n_col, int M, int nb, void* stream) {
     if (!band || !rhs || n_col < 1 || M < 1 || nb < 1) return fail("bad band_solve arguments");
     k_band_solve<<<(n_col + 127) / 128, 128, 0, (cudaStream_t)stream>>>(band, rhs, n_col, M, nb);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+// ---- 3D-IMEX operators (imex3d.cuh) ----------------------------------------
+static I3Args i3args(const hevi_plan* pl, double lam) {
+    I3Args a;
+    a.g = pl->g;
+    a.lv = pl->lv;
+    a.ph = pl->ph;
+    a.cx = pl->cx;
+    a.cy = pl->cy;
+    a.cz = pl->cz;
+    a.Dx = pl->Dx;
+    a.Dy = pl->Dy;
+    a.Dz = pl->Dz;
+    a.N = pl->N;
+    a.Ny = pl->Ny;
+    a.eqset = pl->eqset;
+    a.ainv_identity = pl->ainv_identity;
+    a.lam = lam;
+    return a;
+}
+
+static int i3blocks(const hevi_plan* pl) {
+    const long long n = (long long)pl->g.Z * pl->g.lY * pl->g.lX;
+    return (int)((n + 255) / 256);
+}
+
+int hevi_linear3(hevi_plan* pl, const double* q, double* out, void* stream) {
+    if (!pl || !q || !out) return fail("null argument");
+    k3_linear<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, 0.0), q, out);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_schur3_up(hevi_plan* pl, double lam, const double* P, double* up, void* stream) {
+    if (!pl || !P || !up) return fail("null argument");
+    k3_up<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, lam), P, up);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_schur3_flux(hevi_plan* pl, double lam, const double* P, const double* vel, double* out,
+                     void* stream) {
+    if (!pl || !P || !vel || !out) return fail("null argument");
+    k3_flux<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, lam), P, vel, out);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_schur3_ua(hevi_plan* pl, double lam, const double* qe, double* ua, double* Pe, void* stream) {
+    if (!pl || !qe || !ua || !Pe) return fail("null argument");
+    k3_ua<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, lam), qe, ua, Pe);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_schur3_extract(hevi_plan* pl, double lam, const double* P, const double* ua,
+                        const double* up, const double* qe, double* q, void* stream) {
+    if (!pl || !P || !ua || !up || !qe || !q) return fail("null argument");
+    k3_extract<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, lam), P, ua, up, qe, q);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_wdot(const hevi_plan* pl, const double* x, const double* y, double* out_host, void* stream) {
+    if (!pl || !x || !y || !out_host) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    double* d;
+    CK(cudaMallocAsync(&d, sizeof(double) * (KV_BLOCKS + 1), st));
+    k3_wdot<<<KV_BLOCKS, KV_T, 0, st>>>(pl->g, pl->N, pl->Ny, x, y, d);
+    CK(cudaGetLastError());
+    k3_sum<<<1, 32, 0, st>>>(d, KV_BLOCKS, d + KV_BLOCKS);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_host, d + KV_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d, st));
+    CK(cudaStreamSynchronize(st));
+    return HEVI_OK;
+}
+
+int hevi_axpby(long long n, double alpha, const double* x, double beta, double* y, void* stream) {
+    if (!x || !y || n < 0) return fail("bad axpby arguments");
+    if (n == 0) return HEVI_OK;
+    const long long b = (n + 255) / 256;
+    k3_axpby<<<(int)(b < 1184 ? b : 1184), 256, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y);
     CK(cudaGetLastError());
     return HEVI_OK;
 }

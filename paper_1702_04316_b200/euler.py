@@ -3,12 +3,12 @@
 Same entry points and argument meaning as the reference
 (/root/reference/pkg/src/dycore/euler.py): ``GasConstants``,
 ``hydrostatic_reference``, ``isothermal_reference``, ``build_discretization``,
-``nonlinear_rhs``, ``vertical_restriction``, ``linear_operator``
-(``vertical_only=True``), ``linearized_pressure``, ``equation_of_state``.
+``nonlinear_rhs``, ``vertical_restriction``, ``linear_operator`` (vertical
+or full 3D), ``linearized_pressure``, ``equation_of_state``.
 Arrays in and out are E-vectors ``(5, nel, nqt, nqs, nqr)`` (numpy or torch);
 the arithmetic runs in libhevi.so on the GPU.  Supported: cG, ``set2nc``
-(primary) and ``set2c`` (conservative flux form).  dG and the full 3D linear
-operator are outside the north-star path and raise ``NotImplementedError``.
+(primary) and ``set2c`` (conservative flux form).  dG is outside the device
+path and raises ``NotImplementedError``.
 """
 from __future__ import annotations
 
@@ -214,12 +214,11 @@ def nonlinear_rhs(q, ref: ReferenceState, disc: Discretization, set_name: str,
 
 def linear_operator(q, ref: ReferenceState, disc: Discretization, set_name: str,
                     vertical_only: bool = False, dg: bool = False):
-    """Only the vertical restriction is on the HEVI path (euler.py:313-365)."""
+    """L(q) with DSS-projected derivatives (euler.py:313-365): the vertical
+    restriction (HEVI, ``hevi_linear_v``) or the full 3D operator (3D-IMEX,
+    ``hevi_linear3``)."""
     _check_set(set_name, dg)
-    if not vertical_only:
-        raise NotImplementedError("the full 3D linear operator belongs to 3D-IMEX "
-                                  "(SURVEY 8(f) 'next')")
-    return disc.plan_for(ref, set_name).apply_evec("linear", q)
+    return disc.plan_for(ref, set_name).apply_evec("linear" if vertical_only else "linear3", q)
 
 
 def vertical_restriction(q, ref: ReferenceState, disc: Discretization, set_name: str):

@@ -114,7 +114,8 @@ def rk35_step(q, dt: float, rhs):
 
 @dataclass
 class SolverSpec:
-    """imexcore.py:133-140 (only method='direct' is on the HEVI path)."""
+    """imexcore.py:133-140: 'direct' (1D, fused column solve) or the Krylov
+    solvers 'gmres' | 'bicgstab' | 'richardson' (3D Schur form)."""
     method: str = "gmres"
     tol: float = 1e-6
     max_iter: int = 2000
@@ -131,12 +132,20 @@ class SolveStats:
     matvecs: int = 0
     failures: int = 0
 
+    def add(self, rep):
+        self.solves += 1
+        self.iterations += rep.iterations
+        self.matvecs += rep.matvecs
+        if not rep.converged:
+            self.failures += 1
+
 
 class SolverFailure(RuntimeError):
     """imexcore.py:158-162 (raised by iterative solvers only)."""
 
     def __init__(self, report):
-        super().__init__(f"implicit solve failed: {report}")
+        super().__init__(f"implicit solve failed: iterations={report.iterations} "
+                         f"residual={report.residual:.3e} {report.note}")
         self.report = report
 
 
@@ -153,6 +162,7 @@ class ImplicitProblem:
     solver: SolverSpec = field(default_factory=SolverSpec)
     stats: SolveStats = field(default_factory=SolveStats)
     _column_cache: dict = field(default_factory=dict)
+    _pbno_cache: dict = field(default_factory=dict)
 
     def __post_init__(self):
         if self.discretization == "dg":
@@ -189,14 +199,89 @@ class ImplicitProblem:
         return euler.linear_operator(q, self.ref, self.disc, self.set_name)
 
     def solve(self, q_e):
-        """imexcore.py:312-322 (direct branch)."""
+        """imexcore.py:312-356: the direct column solve (dim='1d') or a Krylov
+        solve of the 3D pressure equation (dim='3d', form='schur')."""
         if self.lam <= 0:
             raise ValueError("implicit solve requires positive lam")
+        if self.solver.method != "direct":
+            return self._solve_krylov(q_e)
         self._check_path()
         from . import columnsolve
         out = columnsolve.solve_direct(self, q_e)
         self.stats.solves += 1
         return out
+
+
+    # -- 3D-IMEX Schur form (imexcore.py:229-298, 324-373) ----------------------
+    def _krylov_path(self):
+        if self.discretization != "cg":
+            raise NotImplementedError("dG is outside the device path")
+        if self.solver.method not in ("gmres", "bicgstab", "richardson"):
+            raise ValueError(f"unknown solver {self.solver.method!r}")
+        if self.dim != "3d":
+            raise NotImplementedError("Krylov solves run the 3D (dim='3d') pressure form; "
+                                      "1D uses method='direct'")
+        if self.form != "schur":
+            raise NotImplementedError("the device Krylov path implements the Schur form")
+        euler._check_set(self.set_name)
+
+    def _solve_krylov(self, q_e):
+        from . import krylov
+        from .plan import to_device
+        self._krylov_path()
+        plan = self.disc.plan_for(self.ref, self.set_name)
+        lam = float(self.lam)
+        E, back = to_device(q_e)
+        if E.shape != (5,) + tuple(self.disc.mesh.nshape):
+            raise ValueError("field/mesh shape mismatch")
+        Qe = plan.e2l(E)
+        ua = plan.zeros(3)
+        Pe = plan.zeros(1)[0]
+        plan.schur3_ua(lam, Qe, ua, Pe)
+        rhs = plan.schur3_flux(lam, Pe, ua, plan.zeros(1)[0])
+        up = plan.zeros(3)
+
+        def lhs_schur(v):
+            plan.schur3_up(lam, v, up)
+            return plan.schur3_flux(lam, v, up, plan.zeros(1)[0])
+
+        amap = krylov.LinearMap(int(np.prod(self.disc.mesh.nshape)), lhs_schur,
+                                space=krylov.LatticeSpace(plan))
+        x, rep = self._run_krylov(amap, rhs, Pe)
+        self.stats.add(rep)
+        if not rep.converged:
+            raise SolverFailure(rep)
+        plan.schur3_up(lam, x, up)
+        q = plan.schur3_extract(lam, x, ua, up, Qe, plan.zeros())
+        return back(plan.l2e(q))
+
+    def _get_pbno(self, amap, order, like):
+        from . import krylov
+        key = (round(self.lam, 12), self.form, self.dim, order, amap.n)
+        if key not in self._pbno_cache:
+            try:
+                self._pbno_cache[key] = krylov.build_pbno(amap, order, like=like)
+            except ValueError:
+                self._pbno_cache[key] = None     # indefinite estimate: unpreconditioned
+        return self._pbno_cache[key]
+
+    def _run_krylov(self, amap, b, x0):
+        """imexcore.py:358-373."""
+        from . import krylov
+        spec = self.solver
+        pre = None
+        if spec.precon_order >= 0 and spec.method in ("bicgstab", "richardson"):
+            pre = self._get_pbno(amap, spec.precon_order, b)
+        elif spec.precon_order > 0:
+            pre = self._get_pbno(amap, spec.precon_order, b)
+        if spec.method == "gmres":
+            return krylov.gmres(amap, b, tol=spec.tol, max_iter=spec.max_iter,
+                                restart=spec.restart, precon=pre, x0=x0)
+        if spec.method == "bicgstab":
+            return krylov.bicgstab_pbno(amap, b, tol=spec.tol, max_iter=spec.max_iter,
+                                        precon=pre, x0=x0)
+        return krylov.richardson_pbno(amap, b, tol=spec.tol, max_iter=spec.max_iter,
+                                      precon=pre, x0=x0, check_every=spec.check_every)
 
 
 def _is_fused(problem, rhs) -> bool:

@@ -28,9 +28,7 @@ def raise_for_flags(flags: int):
     if flags & nv.F_AINV:
         raise FloatingPointError("rank-one inverse denominator underflow")
     if flags & nv.F_PIVOT:
-        raise RuntimeError("no-pivot LU hit a degenerate diagonal (the pivoted dense "
-                           "fallback of columnsolve.factor_with_fallback is not implemented "
-                           "on the device path)")
+        raise RuntimeError("no-pivot LU hit a degenerate diagonal")
     if flags & nv.F_NONFINITE_OUT:
         raise FloatingPointError("non-finite state after IMEX step")
 
@@ -172,6 +170,41 @@ class HeviPlan:
     def stage_solve(self, s, lam, work):
         nv.check(self.lib.hevi_stage_solve(self.h, s, float(lam), nv.ptr(work), nv.stream_ptr()))
 
+    # -- 3D-IMEX operators (imex3d.cuh) ------------------------------------------
+    def linear3(self, q, out):
+        nv.check(self.lib.hevi_linear3(self.h, nv.ptr(q), nv.ptr(out), nv.stream_ptr()))
+        return out
+
+    def schur3_up(self, lam, P, up):
+        nv.check(self.lib.hevi_schur3_up(self.h, float(lam), nv.ptr(P), nv.ptr(up), nv.stream_ptr()))
+        return up
+
+    def schur3_flux(self, lam, P, vel, out):
+        nv.check(self.lib.hevi_schur3_flux(self.h, float(lam), nv.ptr(P), nv.ptr(vel), nv.ptr(out),
+                                           nv.stream_ptr()))
+        return out
+
+    def schur3_ua(self, lam, qe, ua, Pe):
+        nv.check(self.lib.hevi_schur3_ua(self.h, float(lam), nv.ptr(qe), nv.ptr(ua), nv.ptr(Pe),
+                                         nv.stream_ptr()))
+
+    def schur3_extract(self, lam, P, ua, up, qe, q):
+        nv.check(self.lib.hevi_schur3_extract(self.h, float(lam), nv.ptr(P), nv.ptr(ua), nv.ptr(up),
+                                              nv.ptr(qe), nv.ptr(q), nv.stream_ptr()))
+        return q
+
+    def wdot(self, x, y) -> float:
+        out = np.zeros(1)
+        nv.check(self.lib.hevi_wdot(self.h, nv.ptr(x), nv.ptr(y), out.ctypes.data_as(ctypes.c_void_p),
+                                    nv.stream_ptr()))
+        return float(out[0])
+
+    def axpby(self, alpha, x, beta, y):
+        """y <- alpha x + beta y (whole padded arrays)."""
+        nv.check(self.lib.hevi_axpby(y.numel(), float(alpha), nv.ptr(x), float(beta), nv.ptr(y),
+                                     nv.stream_ptr()))
+        return y
+
     def flags(self, reset=True) -> int:
         f = ctypes.c_uint(0)
         nv.check(self.lib.hevi_flags(self.h, ctypes.byref(f), int(reset), nv.stream_ptr()))
@@ -191,6 +224,8 @@ class HeviPlan:
             self.rhs(L, out)
         elif op == "linear":
             self.linear(L, out)
+        elif op == "linear3":
+            self.linear3(L, out)
         elif op == "solve":
             self.solve(lam, L, out)
         else:

@@ -1,0 +1,75 @@
+"""Golden fixtures of the reference's 3D-IMEX path (ImplicitProblem with
+dim="3d", form="schur", Krylov solvers + PBNO; SURVEY 8(d) config 4 /
+8(f) rank 1), made by the UNMODIFIED reference:
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_imex3d_golden.py
+
+Per case (isotropic 3D box, 3x3x3 elements, N=4, both equation sets):
+full linear operator L(q), Schur rhs, lhs_schur(P), Krylov solves
+(GMRES no preconditioner, GMRES + PBNO(1), BiCGstab + PBNO(3), Richardson +
+PBNO(1)) with their iteration counts, and 3 ARK2 3D-IMEX steps."""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from make_golden import (HERE, box3d_mesh, bubble_state, continuous_random_state, dt_for,  # noqa: E402
+                         euler, imx, lattice_index, to_lattice)
+
+SOLVES = {
+    "gmres0": dict(method="gmres", tol=1e-11, precon_order=0),
+    "gmres1": dict(method="gmres", tol=1e-11, precon_order=1),
+    "bicg3": dict(method="bicgstab", tol=1e-11, precon_order=3),
+    "rich1": dict(method="richardson", tol=1e-9, precon_order=1),
+}
+
+
+def run(name, set_name, lam=0.4, C=4.0, nsteps=3):
+    mesh = box3d_mesh(3, 3, 3, 1200.0, 1200.0, 1200.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rep, dims, _ = lattice_index(mesh, 4)
+    L = lambda f: to_lattice(f, rep, dims)  # noqa: E731
+    out = {}
+    qr = continuous_random_state(disc, ref, 21, slab=False)
+    out["ops_q"] = L(qr)
+    out["ops_L3"] = L(euler.linear_operator(qr, ref, disc, set_name))
+    prob = imx.ImplicitProblem(disc=disc, ref=ref, set_name=set_name, form="schur", dim="3d")
+    prob.lam = lam
+    out["ops_lam"] = np.array(lam)
+    rhsP, ua = prob.rhs_schur_build(qr)
+    out["ops_schur_rhs"] = L(rhsP)
+    out["ops_ua"] = L(np.moveaxis(ua, -1, 0))
+    P = euler.linearized_pressure(qr, ref, set_name)
+    out["ops_P"] = L(P)
+    out["ops_lhs"] = L(prob.lhs_schur(P))
+    for tag, spec in SOLVES.items():
+        p = imx.ImplicitProblem(disc=disc, ref=ref, set_name=set_name, form="schur", dim="3d",
+                                solver=imx.SolverSpec(**spec))
+        p.lam = lam
+        out[f"solve_{tag}"] = L(p.solve(qr))
+        out[f"iters_{tag}"] = np.array(p.stats.iterations)
+        out[f"matvecs_{tag}"] = np.array(p.stats.matvecs)
+    q = bubble_state(mesh, ref, disc, 0.5, (600.0, 600.0, 350.0), (250.0, 250.0, 250.0),
+                     slab=False, set_name=set_name)
+    dt = dt_for(mesh, ref, disc, q, C, set_name)
+    out["step_q0"] = L(q)
+    out["step_dt"] = np.array(dt)
+    prob = imx.ImplicitProblem(disc=disc, ref=ref, set_name=set_name, form="schur", dim="3d",
+                               solver=imx.SolverSpec(method="gmres", tol=1e-11, precon_order=1))
+    rhs = lambda s: euler.nonlinear_rhs(s, ref, disc, set_name)  # noqa: E731
+    tab = imx.ark2_tableau()
+    for k in range(1, nsteps + 1):
+        q = imx.ark_imex_step(q, dt, tab, prob, rhs)
+        out[f"step_q{k}"] = L(q)
+    out["step_iters"] = np.array(prob.stats.iterations)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "dt", dt, {k: int(v) for k, v in out.items() if k.startswith(("iters", "step_it"))})
+
+
+if __name__ == "__main__":
+    run("imex3d_box", "set2nc")
+    run("imex3d_box_c", "set2c")

@@ -80,3 +80,20 @@ def test_oracle_pivoted_fallback_matches_banded():
         q, qp = o.step(q, dt), op.step(qp, dt)
     assert isinstance(op.factors(0.3, True)[0], str)
     assert max(rel_fields(o.to_lattice(qp), o.to_lattice(q))) < 1e-12
+
+
+@pytest.mark.parametrize("name,sn", [("imex3d_box", "set2nc"), ("imex3d_box_c", "set2c")])
+def test_oracle_3d_imex_operators_match_reference(name, sn):
+    """Full linear operator and 3D Schur pieces (dim='3d') against the
+    reference goldens of tests/golden/make_imex3d_golden.py."""
+    from oracle.hevi_oracle import BoxOracle
+    g = load_golden(name)
+    o = BoxOracle(3, 3, 3, 1200.0, 1200.0, 1200.0, 4, set_name=sn)
+    q = o.from_lattice(g["ops_q"])
+    lam = float(g["ops_lam"])
+    assert max(rel_fields(o.to_lattice(o.linear3(q)), g["ops_L3"])) < 1e-13
+    rhs, ua = o.schur_rhs3(q, lam)
+    L1 = lambda f: o.to_lattice(np.broadcast_to(f, (5,) + f.shape))[0]  # noqa: E731
+    for got, want in ((L1(rhs), g["ops_schur_rhs"]), (L1(o.lhs_schur3(o.from_lattice(
+            np.broadcast_to(g["ops_P"], (5,) + g["ops_P"].shape))[0], lam)), g["ops_lhs"])):
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
