@@ -136,14 +136,17 @@ int hevi_flags(hevi_plan *plan, unsigned *flags, int reset, void *stream);
  *   hevi_schur3_flux     out = P - _helmholtz_flux(vel)             (:259-268)
  *                        (lhs_schur with vel = up; the Schur rhs with P = Pe, vel = ua)
  *   hevi_schur3_ua       ua, Pe of rhs_schur_build                  (:229-243)
+ * vertical_only != 0 gives the dim = "1d" operators (grad_vc / div_vc,
+ * euler.py:292-300) for Krylov solves of the 1D form.
  *   hevi_schur3_extract  q = extract_from_pressure(P, ua, q_e), up = _up(P)  (:273-298)
  * Krylov vector kernels (krylov.py): hevi_wdot = the E-vector dot product of
  * two continuous lattice fields (multiplicity-weighted, deterministic order);
  * hevi_axpby: y = alpha x + beta y over n doubles. */
 int hevi_linear3(hevi_plan *plan, const double *q, double *out, void *stream);
-int hevi_schur3_up(hevi_plan *plan, double lam, const double *P, double *up, void *stream);
-int hevi_schur3_flux(hevi_plan *plan, double lam, const double *P, const double *vel, double *out,
-                     void *stream);
+int hevi_schur3_up(hevi_plan *plan, double lam, int vertical_only, const double *P, double *up,
+                   void *stream);
+int hevi_schur3_flux(hevi_plan *plan, double lam, int vertical_only, const double *P,
+                     const double *vel, double *out, void *stream);
 int hevi_schur3_ua(hevi_plan *plan, double lam, const double *qe, double *ua, double *Pe, void *stream);
 int hevi_schur3_extract(hevi_plan *plan, double lam, const double *P, const double *ua,
                         const double *up, const double *qe, double *q, void *stream);

@@ -2077,6 +2077,7 @@ static I3Args i3args(const hevi_plan* pl, double lam) {
     a.Ny = pl->Ny;
     a.eqset = pl->eqset;
     a.ainv_identity = pl->ainv_identity;
+    a.vert_only = 0;
     a.lam = lam;
     return a;
 }
@@ -2093,17 +2094,22 @@ int hevi_linear3(hevi_plan* pl, const double* q, double* out, void* stream) {
     return HEVI_OK;
 }
 
-int hevi_schur3_up(hevi_plan* pl, double lam, const double* P, double* up, void* stream) {
+int hevi_schur3_up(hevi_plan* pl, double lam, int vertical_only, const double* P, double* up,
+                   void* stream) {
     if (!pl || !P || !up) return fail("null argument");
-    k3_up<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, lam), P, up);
+    I3Args a = i3args(pl, lam);
+    a.vert_only = vertical_only != 0;
+    k3_up<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(a, P, up);
     CK(cudaGetLastError());
     return HEVI_OK;
 }
 
-int hevi_schur3_flux(hevi_plan* pl, double lam, const double* P, const double* vel, double* out,
-                     void* stream) {
+int hevi_schur3_flux(hevi_plan* pl, double lam, int vertical_only, const double* P, const double* vel,
+                     double* out, void* stream) {
     if (!pl || !P || !vel || !out) return fail("null argument");
-    k3_flux<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, lam), P, vel, out);
+    I3Args a = i3args(pl, lam);
+    a.vert_only = vertical_only != 0;
+    k3_flux<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(a, P, vel, out);
     CK(cudaGetLastError());
     return HEVI_OK;
 }

@@ -28,6 +28,7 @@ struct I3Args {
     Phys ph;
     const double *cx, *cy, *cz, *Dx, *Dy, *Dz;
     int N, Ny, eqset, ainv_identity;
+    int vert_only;   // dim = "1d": grad_vc / div_vc (euler.py:292-300) instead of gradc / divc
     double lam;
 };
 
@@ -82,10 +83,15 @@ __device__ __forceinline__ void grad3(const I3Args& a, const P3& p, S&& s, doubl
                                       double& gz) {
     const Geo& g = a.g;
     const long long sx = 1, sy = g.px, sz = (long long)g.lY * g.px;
-    gx = __ldg(a.cx + p.gx) *
-         fold_d([&](int j) { return s(p.o + (j - p.gx) * sx, p.gz); }, p.gx, a.N, g.nex, a.Dx);
-    gy = __ldg(a.cy + p.gy) *
-         fold_d([&](int j) { return s(p.o + (j - p.gy) * sy, p.gz); }, p.gy, a.Ny, g.ney, a.Dy);
+    if (a.vert_only) {
+        gx = 0.0;
+        gy = 0.0;
+    } else {
+        gx = __ldg(a.cx + p.gx) *
+             fold_d([&](int j) { return s(p.o + (j - p.gx) * sx, p.gz); }, p.gx, a.N, g.nex, a.Dx);
+        gy = __ldg(a.cy + p.gy) *
+             fold_d([&](int j) { return s(p.o + (j - p.gy) * sy, p.gz); }, p.gy, a.Ny, g.ney, a.Dy);
+    }
     gz = __ldg(a.cz + p.gz) *
          fold_d([&](int j) { return s(p.o + (j - p.gz) * sz, j); }, p.gz, a.N, g.nez, a.Dz);
 }
@@ -94,6 +100,9 @@ __device__ __forceinline__ void grad3(const I3Args& a, const P3& p, S&& s, doubl
 __device__ __forceinline__ double div3(const I3Args& a, const P3& p, const double* __restrict__ v) {
     const Geo& g = a.g;
     const long long fs = g.fs, sy = g.px, sz = (long long)g.lY * g.px;
+    if (a.vert_only)
+        return __ldg(a.cz + p.gz) *
+            fold_d([&](int j) { return __ldg(v + 2 * fs + p.o + (j - p.gz) * sz); }, p.gz, a.N, g.nez, a.Dz);
     const double dx = __ldg(a.cx + p.gx) *
         fold_d([&](int j) { return __ldg(v + p.o + (j - p.gx)); }, p.gx, a.N, g.nex, a.Dx);
     const double dy = __ldg(a.cy + p.gy) *

@@ -11,9 +11,10 @@ Shu-Osher launches, BDF2 steps the reference stage loop over the device
 operators; diagnostics are one device reduction per record
 (``hevi_diagnostics``); the E-vector is materialised only for the final
 snapshot.  Supported: box meshes (``case = bubble | rest-state``), cG,
-``set2nc``/``set2c``, ``imex = 1d`` with ``solver = direct`` (Schur form) or
-``integrator = rk35``.  The cubed-sphere acoustic case, dG, 3D-IMEX and the
-Krylov solvers are outside this build and raise ``NotImplementedError``.
+``set2nc``/``set2c``, ``integrator = rk35``, and ARK2 / BDF2 with the Schur
+form: ``imex = 1d, solver = direct`` (fused column solve) or the Krylov
+solvers on either form (``imex = 1d | 3d``).  The cubed-sphere acoustic case,
+dG and the standard (5-variable) form raise ``NotImplementedError``.
 
     python -m paper_1702_04316_b200.driver run <config> [--key=value ...]
 """
@@ -124,12 +125,8 @@ def _check_supported(cfg: RunConfig):
         raise NotImplementedError("the cubed-sphere acoustic case is outside the box-mesh path")
     if cfg.disc != "cg":
         raise NotImplementedError("dG is outside the HEVI direct path")
-    if cfg.integrator in ("ark2", "bdf2"):
-        if cfg.imex != "1d" or cfg.solver != "direct":
-            raise NotImplementedError("3D-IMEX / Krylov solvers are SURVEY 8(f) 'next'; "
-                                      "use imex=1d solver=direct")
-        if cfg.form != "schur":
-            raise NotImplementedError("the device path implements the Schur (pressure) form")
+    if cfg.integrator in ("ark2", "bdf2") and cfg.form != "schur":
+        raise NotImplementedError("the device path implements the Schur (pressure) form")
 
 
 # ---------------------------------------------------------------------------
@@ -305,8 +302,10 @@ def run_simulation(cfg: RunConfig, quiet=False) -> RunResult:
     if cfg.integrator in ("ark2", "bdf2"):
         problem = imexcore.ImplicitProblem(
             disc=disc, ref=ref, set_name=set_name, discretization=cfg.disc, form=cfg.form,
-            dim="1d", solver=imexcore.SolverSpec(method=cfg.solver, tol=cfg.tolerance,
-                                                 precon_order=cfg.precon_order))
+            dim="1d" if cfg.imex == "1d" else "3d",
+            solver=imexcore.SolverSpec(method=cfg.solver, tol=cfg.tolerance,
+                                       precon_order=cfg.precon_order))
+    fused = problem is not None and problem.fused
     ark = imexcore.ark2_tableau()
     tarr = tableau_array(ark)
     bdf = imexcore.bdf2_coefficients()
@@ -336,6 +335,13 @@ def run_simulation(cfg: RunConfig, quiet=False) -> RunResult:
             if cfg.integrator == "rk35":
                 plan.rk35(step_dt, Q, work)
                 plan.check_flags()
+            elif not fused and (cfg.integrator == "ark2" or q_prev is None or step_dt != dt):
+                # Krylov solves: the reference stage loop over the device operators
+                qn = plan.l2e(Q)
+                qn1 = imexcore.ark_imex_step(qn, step_dt, ark, problem, rhs)
+                if cfg.integrator == "bdf2":
+                    q_prev = qn
+                plan.e2l(qn1, out=Q)
             elif cfg.integrator == "ark2" or q_prev is None or step_dt != dt:
                 if cfg.integrator == "bdf2":
                     q_prev = plan.l2e(Q)

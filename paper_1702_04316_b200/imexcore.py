@@ -218,9 +218,8 @@ class ImplicitProblem:
             raise NotImplementedError("dG is outside the device path")
         if self.solver.method not in ("gmres", "bicgstab", "richardson"):
             raise ValueError(f"unknown solver {self.solver.method!r}")
-        if self.dim != "3d":
-            raise NotImplementedError("Krylov solves run the 3D (dim='3d') pressure form; "
-                                      "1D uses method='direct'")
+        if self.dim not in ("1d", "3d"):
+            raise ValueError(f"unknown dim {self.dim!r}")
         if self.form != "schur":
             raise NotImplementedError("the device Krylov path implements the Schur form")
         euler._check_set(self.set_name)
@@ -235,15 +234,16 @@ class ImplicitProblem:
         if E.shape != (5,) + tuple(self.disc.mesh.nshape):
             raise ValueError("field/mesh shape mismatch")
         Qe = plan.e2l(E)
+        vo = self.dim == "1d"          # grad_vc / div_vc instead of gradc / divc
         ua = plan.zeros(3)
         Pe = plan.zeros(1)[0]
         plan.schur3_ua(lam, Qe, ua, Pe)
-        rhs = plan.schur3_flux(lam, Pe, ua, plan.zeros(1)[0])
+        rhs = plan.schur3_flux(lam, Pe, ua, plan.zeros(1)[0], vo)
         up = plan.zeros(3)
 
         def lhs_schur(v):
-            plan.schur3_up(lam, v, up)
-            return plan.schur3_flux(lam, v, up, plan.zeros(1)[0])
+            plan.schur3_up(lam, v, up, vo)
+            return plan.schur3_flux(lam, v, up, plan.zeros(1)[0], vo)
 
         amap = krylov.LinearMap(int(np.prod(self.disc.mesh.nshape)), lhs_schur,
                                 space=krylov.LatticeSpace(plan))
@@ -251,7 +251,7 @@ class ImplicitProblem:
         self.stats.add(rep)
         if not rep.converged:
             raise SolverFailure(rep)
-        plan.schur3_up(lam, x, up)
+        plan.schur3_up(lam, x, up, vo)
         q = plan.schur3_extract(lam, x, ua, up, Qe, plan.zeros())
         return back(plan.l2e(q))
 

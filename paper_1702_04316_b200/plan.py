@@ -175,13 +175,14 @@ class HeviPlan:
         nv.check(self.lib.hevi_linear3(self.h, nv.ptr(q), nv.ptr(out), nv.stream_ptr()))
         return out
 
-    def schur3_up(self, lam, P, up):
-        nv.check(self.lib.hevi_schur3_up(self.h, float(lam), nv.ptr(P), nv.ptr(up), nv.stream_ptr()))
+    def schur3_up(self, lam, P, up, vertical_only=False):
+        nv.check(self.lib.hevi_schur3_up(self.h, float(lam), int(vertical_only), nv.ptr(P), nv.ptr(up),
+                                         nv.stream_ptr()))
         return up
 
-    def schur3_flux(self, lam, P, vel, out):
-        nv.check(self.lib.hevi_schur3_flux(self.h, float(lam), nv.ptr(P), nv.ptr(vel), nv.ptr(out),
-                                           nv.stream_ptr()))
+    def schur3_flux(self, lam, P, vel, out, vertical_only=False):
+        nv.check(self.lib.hevi_schur3_flux(self.h, float(lam), int(vertical_only), nv.ptr(P),
+                                           nv.ptr(vel), nv.ptr(out), nv.stream_ptr()))
         return out
 
     def schur3_ua(self, lam, qe, ua, Pe):

@@ -30,6 +30,10 @@ CASES = {
                "--nx=4", "--nz=4", "--courant=2", "--end_time=1.0"],
     "ark2_rest": ["--case=rest-state", "--integrator=ark2", "--imex=1d", "--solver=direct",
                   "--nx=3", "--nz=3", "--courant=3", "--end_time=0.5", "--diag_interval=0.2"],
+    "ark2_3d": ["--integrator=ark2", "--imex=3d", "--solver=gmres", "--tolerance=1e-10",
+                "--nx=4", "--nz=4", "--courant=2", "--end_time=0.6"],
+    "bdf2_3d_bicg": ["--integrator=bdf2", "--imex=3d", "--solver=bicgstab", "--precon_order=3",
+                     "--tolerance=1e-10", "--nx=4", "--nz=4", "--courant=2", "--end_time=0.8"],
 }
 
 
@@ -45,8 +49,9 @@ def main():
         np.savez_compressed(os.path.join(HERE, f"driver_{name}.npz"), overrides=np.array(ov),
                             ts=np.array([list(r) for r in ts]), csv=np.array(csv_text),
                             snapshot=snap, snapshot_name=np.array(snaps[0]), dt=res.dt,
-                            steps=res.steps, solves=res.stats.solves, exit_code=res.exit_code)
-        print(name, res.steps, res.dt, res.exit_code, res.stats.solves)
+                            steps=res.steps, solves=res.stats.solves, exit_code=res.exit_code,
+                            iterations=res.stats.iterations)
+        print(name, res.steps, res.dt, res.exit_code, res.stats.solves, res.stats.iterations)
 
 
 if __name__ == "__main__":

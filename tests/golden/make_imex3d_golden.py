@@ -2,7 +2,7 @@
 dim="3d", form="schur", Krylov solvers + PBNO; SURVEY 8(d) config 4 /
 8(f) rank 1), made by the UNMODIFIED reference:
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_imex3d_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_imex3d_golden.py [--1d]
 
 Per case (isotropic 3D box, 3x3x3 elements, N=4, both equation sets):
 full linear operator L(q), Schur rhs, lhs_schur(P), Krylov solves
@@ -70,6 +70,38 @@ def run(name, set_name, lam=0.4, C=4.0, nsteps=3):
     print(name, "dt", dt, {k: int(v) for k, v in out.items() if k.startswith(("iters", "step_it"))})
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--1d" not in sys.argv:
     run("imex3d_box", "set2nc")
     run("imex3d_box_c", "set2c")
+
+
+def run_1d(name="krylov1d_slab"):
+    """Krylov solves of the 1D form (dim='1d', grad_vc/div_vc) on the slab_aniso
+    case (test_columnsolve.py:240-252: direct == GMRES to 1e-8 at lam = 0.8)."""
+    from make_golden import sg
+    mesh = sg.build_box_mesh(5, 4, 20_000.0, 1000.0, 4)
+    mesh.meta["ny"] = 1
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rep, dims, _ = lattice_index(mesh, 1)
+    L = lambda f: to_lattice(f, rep, dims)  # noqa: E731
+    qr = continuous_random_state(disc, ref, 32, slab=True)
+    out = {"ops_q": L(qr), "ops_lam": np.array(0.8)}
+    for tag, spec in {"gmres0": dict(method="gmres", tol=1e-12, precon_order=0),
+                      "gmres1": dict(method="gmres", tol=1e-12, precon_order=1),
+                      "bicg3": dict(method="bicgstab", tol=1e-12, precon_order=3)}.items():
+        p = imx.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="schur", dim="1d",
+                                solver=imx.SolverSpec(**spec))
+        p.lam = 0.8
+        out[f"solve_{tag}"] = L(p.solve(qr))
+        out[f"iters_{tag}"] = np.array(p.stats.iterations)
+    p = imx.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="schur", dim="1d",
+                            solver=imx.SolverSpec(method="direct"))
+    p.lam = 0.8
+    out["solve_direct"] = L(p.solve(qr))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: int(v) for k, v in out.items() if k.startswith("iters")})
+
+
+if __name__ == "__main__" and "--1d" in sys.argv:
+    run_1d()

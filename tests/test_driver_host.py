@@ -40,8 +40,7 @@ def test_parse_config_defaults_overrides_and_errors(tmp_path):
 
 
 def test_unsupported_paths_raise():
-    for ov in (["--case=acoustic"], ["--integrator=ark2"], ["--integrator=ark2", "--imex=1d",
-                                                             "--solver=gmres"]):
+    for ov in (["--case=acoustic"], ["--integrator=ark2", "--form=standard"]):
         with pytest.raises(NotImplementedError):
             driver._check_supported(driver.parse_config(None, ov))
 

@@ -114,3 +114,31 @@ def test_solver_failure_raises(case):
     with pytest.raises(imexcore.SolverFailure):
         prob.solve(o.from_lattice(g["ops_q"]))
     assert prob.stats.failures == 1
+
+
+@pytest.mark.parametrize("tag", ["gmres0", "gmres1", "bicg3"])
+def test_krylov_1d_form_matches_reference_and_direct(tag):
+    """Krylov solves of the 1D form (grad_vc/div_vc) on the anisotropic slab:
+    reference iteration counts, and direct == GMRES to 1e-8 at lam = 0.8
+    (test_columnsolve.py:240-252)."""
+    from oracle.hevi_oracle import BoxOracle
+    g = np.load(os.path.join(HERE, "golden", "krylov1d_slab.npz"))
+    mesh = specgrid.build_box_mesh(5, 4, 20_000.0, 1000.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    o = BoxOracle(5, 1, 4, 20_000.0, None, 1000.0, 4, slab=True)
+    spec = {"gmres0": dict(method="gmres", tol=1e-12, precon_order=0),
+            "gmres1": dict(method="gmres", tol=1e-12, precon_order=1),
+            "bicg3": dict(method="bicgstab", tol=1e-12, precon_order=3)}[tag]
+    prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="schur", dim="1d",
+                                    solver=imexcore.SolverSpec(**spec))
+    prob.lam = 0.8
+    q = o.from_lattice(g["ops_q"])
+    out = o.to_lattice(prob.solve(q))
+    assert max(rel_fields(out, g[f"solve_{tag}"])) < 1e-9
+    assert max(rel_fields(out, g["solve_direct"])) < 1e-8
+    assert abs(prob.stats.iterations - int(g[f"iters_{tag}"])) <= 1
+    direct = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="schur", dim="1d",
+                                      solver=imexcore.SolverSpec(method="direct"))
+    direct.lam = 0.8
+    assert max(rel_fields(out, o.to_lattice(direct.solve(q)))) < 1e-8

@@ -75,9 +75,6 @@ def test_unsupported_paths_raise_not_implemented():
         euler.nonlinear_rhs(q, ref, disc, "set2c", dg=True)
     with pytest.raises(ValueError):
         euler.nonlinear_rhs(q, ref, disc, "set3")
-    prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="1d", lam=0.3)
-    with pytest.raises(NotImplementedError):          # Krylov solves run the 3D form
-        prob.solve(q)
     prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="3d", lam=0.3,
                                     form="standard")
     with pytest.raises(NotImplementedError):
