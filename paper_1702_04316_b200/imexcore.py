@@ -86,14 +86,12 @@ def rk35_step(q, dt: float, rhs):
     """One SSP RK(5,3) step (imexcore.py:111-126).  With ``rhs`` an
     ``euler.RHS`` the five stages run as fused device launches."""
     if isinstance(rhs, euler.RHS):
-        from .plan import to_device
         plan = rhs.disc.plan_for(rhs.ref, rhs.set_name)
-        E, back = to_device(q)
-        Q = plan.e2l(E)
+        Q, back = plan.lattice_in(q)
         work = plan.workspace()
         plan.rk35(dt, Q, work)
         plan.check_flags()
-        return back(plan.l2e(Q))
+        return back(Q)
     u = [q]
     for i in range(1, 6):
         acc = q * 0.0
@@ -293,16 +291,15 @@ def _is_fused(problem, rhs) -> bool:
 def ark_imex_step(q, dt: float, tableau: ButcherPair, problem, rhs):
     """One additive Runge-Kutta IMEX step (imexcore.py:385-414)."""
     if _is_fused(problem, rhs) and tableau.stages == 3:
-        from .plan import tableau_array, to_device
+        from .plan import tableau_array
         plan = problem.disc.plan_for(problem.ref, problem.set_name)
         problem.lam = tableau.diag * dt
-        E, back = to_device(q)
-        Q = plan.e2l(E)
+        Q, back = plan.lattice_in(q)
         work = plan.workspace()
         plan.step(dt, tableau_array(tableau), Q, work)
         plan.check_flags()
         problem.stats.solves += 2
-        return back(plan.l2e(Q))
+        return back(Q)
     return _generic_step(q, dt, tableau, problem, rhs)
 
 

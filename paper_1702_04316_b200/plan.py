@@ -214,6 +214,18 @@ class HeviPlan:
     def check_flags(self):
         raise_for_flags(self.flags(reset=True))
 
+    # -- reference-facing entry: E-vector in, E-vector out ------------------------
+    def lattice_in(self, q):
+        """E-vector (numpy / torch, host or device) -> (lattice tensor, back),
+        ``back`` returning the result in the caller's array type.  (Gathering
+        the unique copies straight from pinned host memory was measured no
+        faster than the DMA copy: PCIe sectors make the strided gather read
+        as many bytes, profiles/README.md.)"""
+        E, back0 = to_device(q)
+        if E.shape != (5,) + tuple(self.mesh.nshape):
+            raise ValueError("field/mesh shape mismatch")
+        return self.e2l(E), (lambda L: back0(self.l2e(L)))
+
     # -- E-vector entry used by the drop-in operators ---------------------------
     def apply_evec(self, op, q, lam=None):
         E, back = to_device(q)

@@ -186,3 +186,26 @@ def test_direct_solve_cost_flat_in_courant(box3):
     plan = disc.plan_for(ref)
     nbs = {plan.factor(lam) for lam in (0.05, 0.5, 5.0)}
     assert len(nbs) == 1
+
+
+@pytest.mark.parametrize("integrator", ["ark2", "rk35"])
+def test_host_and_device_inputs_give_bitwise_equal_steps(box3, integrator):
+    """Pinned host, device and numpy E-vectors through the fused entry points
+    give the same bits, returned in the caller's array type."""
+    mesh, ref, disc = box3
+    qd = random_continuous(box3, seed=3)
+    qh = torch.empty(qd.shape, dtype=torch.float64, pin_memory=True)
+    qh.copy_(qd)
+    qn = qd.cpu().numpy()
+    rhs = euler.make_rhs(ref, disc, "set2nc")
+    tab = imexcore.ark2_tableau()
+    outs = []
+    for q in (qd, qh, qn):
+        if integrator == "ark2":
+            prob = problem(box3)
+            r = imexcore.ark_imex_step(q, 0.5, tab, prob, rhs)
+        else:
+            r = imexcore.rk35_step(q, 0.05, rhs)
+        outs.append(r.cpu().numpy() if isinstance(r, torch.Tensor) else r)
+    assert isinstance(imexcore.rk35_step(qh, 0.05, rhs), torch.Tensor)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
