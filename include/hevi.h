@@ -140,7 +140,8 @@ int hevi_flags(hevi_plan *plan, unsigned *flags, int reset, void *stream);
  * euler.py:292-300) for Krylov solves of the 1D form.
  *   hevi_schur3_extract  q = extract_from_pressure(P, ua, q_e), up = _up(P)  (:273-298)
  * Krylov vector kernels (krylov.py): hevi_wdot = the E-vector dot product of
- * two continuous lattice fields (multiplicity-weighted, deterministic order);
+ * two continuous lattice states of nf fields (multiplicity-weighted,
+ * deterministic order);
  * hevi_axpby: y = alpha x + beta y over n doubles. */
 int hevi_linear3(hevi_plan *plan, const double *q, double *out, void *stream);
 int hevi_schur3_up(hevi_plan *plan, double lam, int vertical_only, const double *P, double *up,
@@ -150,7 +151,8 @@ int hevi_schur3_flux(hevi_plan *plan, double lam, int vertical_only, const doubl
 int hevi_schur3_ua(hevi_plan *plan, double lam, const double *qe, double *ua, double *Pe, void *stream);
 int hevi_schur3_extract(hevi_plan *plan, double lam, const double *P, const double *ua,
                         const double *up, const double *qe, double *q, void *stream);
-int hevi_wdot(const hevi_plan *plan, const double *x, const double *y, double *out_host, void *stream);
+int hevi_wdot(const hevi_plan *plan, const double *x, const double *y, int nf, double *out_host,
+              void *stream);
 int hevi_axpby(long long n, double alpha, const double *x, double beta, double *y, void *stream);
 
 /* Run diagnostics (bench.total_mass / max_perturbations, bench.py:131-137) of a

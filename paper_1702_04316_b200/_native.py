@@ -76,7 +76,7 @@ SIGNATURES = {
     "hevi_schur3_flux": (_I, [_V, _D, _I, _V, _V, _V, _V]),
     "hevi_schur3_ua": (_I, [_V, _D, _V, _V, _V, _V]),
     "hevi_schur3_extract": (_I, [_V, _D, _V, _V, _V, _V, _V, _V]),
-    "hevi_wdot": (_I, [_V, _V, _V, _V, _V]),
+    "hevi_wdot": (_I, [_V, _V, _V, _I, _V, _V]),
     "hevi_axpby": (_I, [_LL, _D, _V, _D, _V, _V]),
     "hevi_lu_pivot_solve": (_I, [_V, _V, _V, _I, _I, _V]),
     "hevi_plan_set_option": (_I, [_V, _I, _I]),

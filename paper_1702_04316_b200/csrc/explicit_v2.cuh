@@ -24,6 +24,10 @@
 //      L_V(q) pointwise, no-flux projection, fused ARK2 stage epilogue.
 #pragma once
 
+__device__ __forceinline__ void pf_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int N, int NY>
 struct Tile2;   // TX, TY, MINB (defined with the dispatch in hevi.cu)
 

@@ -2129,12 +2129,13 @@ int hevi_schur3_extract(hevi_plan* pl, double lam, const double* P, const double
     return HEVI_OK;
 }
 
-int hevi_wdot(const hevi_plan* pl, const double* x, const double* y, double* out_host, void* stream) {
-    if (!pl || !x || !y || !out_host) return fail("null argument");
+int hevi_wdot(const hevi_plan* pl, const double* x, const double* y, int nf, double* out_host,
+              void* stream) {
+    if (!pl || !x || !y || !out_host || nf < 1) return fail("bad wdot arguments");
     cudaStream_t st = (cudaStream_t)stream;
     double* d;
     CK(cudaMallocAsync(&d, sizeof(double) * (KV_BLOCKS + 1), st));
-    k3_wdot<<<KV_BLOCKS, KV_T, 0, st>>>(pl->g, pl->N, pl->Ny, x, y, d);
+    k3_wdot<<<KV_BLOCKS, KV_T, 0, st>>>(pl->g, pl->N, pl->Ny, nf, x, y, d);
     CK(cudaGetLastError());
     k3_sum<<<1, 32, 0, st>>>(d, KV_BLOCKS, d + KV_BLOCKS);
     CK(cudaGetLastError());

@@ -289,15 +289,15 @@ __device__ __forceinline__ double mult_axis(int gi, int N, int ne) {
     return (gi > 0 && gi < ne * N && gi % N == 0) ? 2.0 : 1.0;
 }
 
-__global__ void k3_wdot(Geo g, int N, int Ny, const double* __restrict__ x, const double* __restrict__ y,
-                        double* part) {
+__global__ void k3_wdot(Geo g, int N, int Ny, int nf, const double* __restrict__ x,
+                        const double* __restrict__ y, double* part) {
     __shared__ double sm[KV_T];
     const long long n = (long long)g.Z * g.lY * g.lX;
     double s = 0.0;
     for (long long i = (long long)blockIdx.x * KV_T + threadIdx.x; i < n; i += (long long)KV_BLOCKS * KV_T) {
         const P3 p = point3(g, i);
         const double m = mult_axis(p.gx, N, g.nex) * mult_axis(p.gy, Ny, g.ney) * mult_axis(p.gz, N, g.nez);
-        s = fma(m * x[p.o], y[p.o], s);
+        for (int f = 0; f < nf; ++f) s = fma(m * x[p.o + f * g.fs], y[p.o + f * g.fs], s);
     }
     sm[threadIdx.x] = s;
     __syncthreads();

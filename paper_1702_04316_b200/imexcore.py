@@ -218,8 +218,8 @@ class ImplicitProblem:
             raise ValueError(f"unknown solver {self.solver.method!r}")
         if self.dim not in ("1d", "3d"):
             raise ValueError(f"unknown dim {self.dim!r}")
-        if self.form != "schur":
-            raise NotImplementedError("the device Krylov path implements the Schur form")
+        if self.form not in ("schur", "standard"):
+            raise ValueError(f"unknown form {self.form!r}")
         euler._check_set(self.set_name)
 
     def _solve_krylov(self, q_e):
@@ -232,6 +232,8 @@ class ImplicitProblem:
         if E.shape != (5,) + tuple(self.disc.mesh.nshape):
             raise ValueError("field/mesh shape mismatch")
         Qe = plan.e2l(E)
+        if self.form == "standard":
+            return back(plan.l2e(self._solve_standard(plan, Qe, lam)))
         vo = self.dim == "1d"          # grad_vc / div_vc instead of gradc / divc
         ua = plan.zeros(3)
         Pe = plan.zeros(1)[0]
@@ -252,6 +254,41 @@ class ImplicitProblem:
         plan.schur3_up(lam, x, up, vo)
         q = plan.schur3_extract(lam, x, ua, up, Qe, plan.zeros())
         return back(plan.l2e(q))
+
+    def _solve_standard(self, plan, Qe, lam):
+        """5-variable form with the reference's per-field diagonal scaling
+        q = D x, D = diag(rho/c, 1, 1, 1, theta/c) (imexcore.py:330-355)."""
+        from . import krylov
+        mesh = self.disc.mesh
+        lev = _node_levels(mesh)
+        cbar = float(np.sqrt(self.ref.G0_nc[lev].mean()))
+        D = np.ones(5)
+        D[0] = float(self.ref.rho0[lev].mean()) / cbar
+        D[4] = float(self.ref.theta0[lev].mean()) / cbar
+        op = plan.linear if self.dim == "1d" else plan.linear3
+
+        def scaled(src, s, dst):
+            for f in range(5):
+                plan.axpby(float(s[f]), src[f], 0.0, dst[f])
+            return dst
+
+        Dinv = 1.0 / D
+
+        def lhs(v):
+            t = scaled(v, D, plan.zeros())
+            Lt = op(t, plan.zeros())
+            plan.axpby(-lam, Lt, 1.0, t)          # q - lam L(q)
+            return scaled(t, Dinv, t)
+
+        amap = krylov.LinearMap(5 * int(np.prod(mesh.nshape)), lhs,
+                                space=krylov.LatticeSpace(plan, nf=5))
+        b = scaled(Qe, Dinv, plan.zeros())
+        x, rep = self._run_krylov(amap, b, b.clone())
+        plan.check_flags()
+        self.stats.add(rep)
+        if not rep.converged:
+            raise SolverFailure(rep)
+        return scaled(x, D, plan.zeros())
 
     def _get_pbno(self, amap, order, like):
         from . import krylov
@@ -280,6 +317,14 @@ class ImplicitProblem:
                                         precon=pre, x0=x0)
         return krylov.richardson_pbno(amap, b, tol=spec.tol, max_iter=spec.max_iter,
                                       precon=pre, x0=x0, check_every=spec.check_every)
+
+
+def _node_levels(mesh):
+    """Level index of every E-vector node (per-node means of level tables)."""
+    nel, nt, ns, nr = mesh.nshape
+    kz = np.arange(nel) // (mesh.nx * mesh.ny)
+    lev = kz[:, None] * mesh.N + np.arange(nt)[None, :]
+    return np.broadcast_to(lev[:, :, None, None], mesh.nshape)
 
 
 def _is_fused(problem, rhs) -> bool:

@@ -194,10 +194,10 @@ class HeviPlan:
                                               nv.ptr(qe), nv.ptr(q), nv.stream_ptr()))
         return q
 
-    def wdot(self, x, y) -> float:
+    def wdot(self, x, y, nf=1) -> float:
         out = np.zeros(1)
-        nv.check(self.lib.hevi_wdot(self.h, nv.ptr(x), nv.ptr(y), out.ctypes.data_as(ctypes.c_void_p),
-                                    nv.stream_ptr()))
+        nv.check(self.lib.hevi_wdot(self.h, nv.ptr(x), nv.ptr(y), int(nf),
+                                    out.ctypes.data_as(ctypes.c_void_p), nv.stream_ptr()))
         return float(out[0])
 
     def axpby(self, alpha, x, beta, y):

@@ -2,7 +2,7 @@
 dim="3d", form="schur", Krylov solvers + PBNO; SURVEY 8(d) config 4 /
 8(f) rank 1), made by the UNMODIFIED reference:
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_imex3d_golden.py [--1d]
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_imex3d_golden.py [--1d | --standard]
 
 Per case (isotropic 3D box, 3x3x3 elements, N=4, both equation sets):
 full linear operator L(q), Schur rhs, lhs_schur(P), Krylov solves
@@ -70,7 +70,7 @@ def run(name, set_name, lam=0.4, C=4.0, nsteps=3):
     print(name, "dt", dt, {k: int(v) for k, v in out.items() if k.startswith(("iters", "step_it"))})
 
 
-if __name__ == "__main__" and "--1d" not in sys.argv:
+if __name__ == "__main__" and "--1d" not in sys.argv and "--standard" not in sys.argv:
     run("imex3d_box", "set2nc")
     run("imex3d_box_c", "set2c")
 
@@ -105,3 +105,40 @@ def run_1d(name="krylov1d_slab"):
 
 if __name__ == "__main__" and "--1d" in sys.argv:
     run_1d()
+
+
+def run_standard(name="krylov_standard"):
+    """Standard (5-variable) form Krylov solves (imexcore.py:330-355) on the 3D
+    box (dim='3d') and on the anisotropic slab (dim='1d')."""
+    from make_golden import sg
+    out = {}
+    mesh = box3d_mesh(3, 3, 3, 1200.0, 1200.0, 1200.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rep, dims, _ = lattice_index(mesh, 4)
+    qr = continuous_random_state(disc, ref, 21, slab=False)
+    out["box_q"] = to_lattice(qr, rep, dims)
+    for sn in ("set2nc", "set2c"):
+        p = imx.ImplicitProblem(disc=disc, ref=ref, set_name=sn, form="standard", dim="3d",
+                                solver=imx.SolverSpec(method="gmres", tol=1e-11, precon_order=1))
+        p.lam = 0.4
+        out[f"box_{sn}"] = to_lattice(p.solve(qr), rep, dims)
+        out[f"box_{sn}_iters"] = np.array(p.stats.iterations)
+    mesh = sg.build_box_mesh(5, 4, 20_000.0, 1000.0, 4)
+    mesh.meta["ny"] = 1
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rep, dims, _ = lattice_index(mesh, 1)
+    qr = continuous_random_state(disc, ref, 32, slab=True)
+    out["slab_q"] = to_lattice(qr, rep, dims)
+    p = imx.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="standard", dim="1d",
+                            solver=imx.SolverSpec(method="bicgstab", tol=1e-11, precon_order=3))
+    p.lam = 0.8
+    out["slab_bicg"] = to_lattice(p.solve(qr), rep, dims)
+    out["slab_bicg_iters"] = np.array(p.stats.iterations)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: int(v) for k, v in out.items() if k.endswith("iters")})
+
+
+if __name__ == "__main__" and "--standard" in sys.argv:
+    run_standard()

@@ -142,3 +142,43 @@ def test_krylov_1d_form_matches_reference_and_direct(tag):
                                       solver=imexcore.SolverSpec(method="direct"))
     direct.lam = 0.8
     assert max(rel_fields(out, o.to_lattice(direct.solve(q)))) < 1e-8
+
+
+@pytest.mark.parametrize("which", ["box_set2nc", "box_set2c", "slab_bicg"])
+def test_standard_form_krylov_matches_reference(which):
+    """5-variable form with the reference's diagonal scaling (imexcore.py:330-355)."""
+    from oracle.hevi_oracle import BoxOracle
+    g = np.load(os.path.join(HERE, "golden", "krylov_standard.npz"))
+    if which.startswith("box"):
+        sn = which[4:]
+        mesh = specgrid.build_box_mesh_3d(3, 3, 3, 1200.0, 1200.0, 1200.0, 4)
+        o = BoxOracle(3, 3, 3, 1200.0, 1200.0, 1200.0, 4, set_name=sn)
+        spec, dim, lam, q = dict(method="gmres", tol=1e-11, precon_order=1), "3d", 0.4, g["box_q"]
+    else:
+        sn = "set2nc"
+        mesh = specgrid.build_box_mesh(5, 4, 20_000.0, 1000.0, 4)
+        o = BoxOracle(5, 1, 4, 20_000.0, None, 1000.0, 4, slab=True)
+        spec, dim, lam, q = dict(method="bicgstab", tol=1e-11, precon_order=3), "1d", 0.8, g["slab_q"]
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name=sn, form="standard", dim=dim,
+                                    solver=imexcore.SolverSpec(**spec))
+    prob.lam = lam
+    out = o.to_lattice(prob.solve(o.from_lattice(q)))
+    errs = rel_fields(out, g[which])
+    print(which, prob.stats.iterations, int(g[f"{which}_iters"]), errs)
+    if which.startswith("box"):
+        assert max(errs) < 1e-8, errs
+    else:
+        # the 1D standard form is ill-conditioned (cond ~5e5, SURVEY 8(a) a17): a
+        # 1e-11 residual leaves ~1e-7 solution error in either implementation,
+        # so both are measured against the exact (direct Schur) solution
+        exact = np.load(os.path.join(HERE, "golden", "krylov1d_slab.npz"))["solve_direct"]
+        e_ref = max(rel_fields(g[which], exact))
+        e_mine = max(rel_fields(out, exact))
+        print("vs exact: reference", e_ref, "device", e_mine)
+        assert e_mine < max(10 * e_ref, 1e-9), (e_mine, e_ref)
+    # PBNO is fitted on Ritz values from a different random start vector; on the
+    # ill-conditioned 1D standard form BiCGstab's count moves with it (95 vs 105)
+    want = int(g[f"{which}_iters"])
+    assert abs(prob.stats.iterations - want) <= max(2, want // (10 if which.startswith("box") else 4))

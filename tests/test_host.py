@@ -76,8 +76,8 @@ def test_unsupported_paths_raise_not_implemented():
     with pytest.raises(ValueError):
         euler.nonlinear_rhs(q, ref, disc, "set3")
     prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="3d", lam=0.3,
-                                    form="standard")
-    with pytest.raises(NotImplementedError):
+                                    form="bogus")
+    with pytest.raises(ValueError):
         prob.solve(q)
     prob = imexcore.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", dim="3d", lam=0.3,
                                     solver=imexcore.SolverSpec(method="direct"))
