@@ -30,6 +30,14 @@ CASES = {
                          slab=True, courant=15.0, set_name="set2c"),
     "box3d_n4_c": dict(nx=4, ny=4, nz=4, Lx=16_000.0, Ly=16_000.0, Lz=400.0, N=4,
                        courant=15.0, set_name="set2c"),
+    # further orders (make_golden.py --extra)
+    "box3d_n5": dict(nx=3, ny=3, nz=3, Lx=15_000.0, Ly=15_000.0, Lz=600.0, N=5, courant=15.0),
+    "box3d_n6_c": dict(nx=3, ny=2, nz=2, Lx=12_000.0, Ly=8_000.0, Lz=400.0, N=6,
+                       courant=15.0, set_name="set2c"),
+    "slab_n2": dict(nx=8, ny=1, nz=6, Lx=16_000.0, Ly=None, Lz=600.0, N=2, slab=True,
+                    courant=15.0),
+    "box3d_n2_iso": dict(nx=4, ny=4, nz=5, Lx=8_000.0, Ly=8_000.0, Lz=500.0, N=2,
+                         background="isothermal", courant=15.0),
 }
 
 

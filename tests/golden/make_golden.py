@@ -273,5 +273,26 @@ def main():
         json.dump(host, f, indent=1)
 
 
+def extra():
+    """Further polynomial orders and stratifications for the parity gates."""
+    mesh = box3d_mesh(3, 3, 3, 15_000.0, 15_000.0, 600.0, 5)
+    run_case("box3d_n5", mesh, 5, False, ops_seed=41, lam=0.3,
+             bubble=(0.5, (7_500.0, 7_500.0, 300.0), (3000.0, 3000.0, 150.0)),
+             C=15.0, nsteps=5, keep=(1, 5))
+    mesh = box3d_mesh(3, 2, 2, 12_000.0, 8_000.0, 400.0, 6)
+    run_case("box3d_n6_c", mesh, 6, False, ops_seed=42, lam=0.3,
+             bubble=(0.5, (6_000.0, 4_000.0, 200.0), (3000.0, 3000.0, 100.0)),
+             C=15.0, nsteps=5, keep=(1, 5), set_name="set2c")
+    mesh = sg.build_box_mesh(8, 6, 16_000.0, 600.0, 2)
+    mesh.meta["ny"] = 1
+    run_case("slab_n2", mesh, 1, True, ops_seed=43, lam=0.5,
+             bubble=(0.5, (8_000.0, 0.0, 300.0), (2000.0, 1.0, 150.0)),
+             C=15.0, nsteps=10, keep=(1, 10))
+    mesh = box3d_mesh(4, 4, 5, 8_000.0, 8_000.0, 500.0, 2)
+    run_case("box3d_n2_iso", mesh, 2, False, ops_seed=44, lam=0.25,
+             bubble=(0.5, (4_000.0, 4_000.0, 250.0), (2000.0, 2000.0, 120.0)),
+             C=15.0, nsteps=5, keep=(1, 5), background="isothermal")
+
+
 if __name__ == "__main__":
-    main()
+    extra() if "--extra" in sys.argv else main()
