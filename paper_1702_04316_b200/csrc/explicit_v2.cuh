@@ -24,6 +24,15 @@
 //      L_V(q) pointwise, no-flux projection, fused ARK2 stage epilogue.
 #pragma once
 
+// Per mode (bit MODE): form the x-face partials of the 5 state fields in the
+// P' phase and let the face points take their own P' face line, which drops
+// one barrier per layer.  Measured at config 5: stage 0 (M_S1) 1.581 -> 1.548
+// ms, stage 2 (M_S3) 1.443 -> 1.402 ms, but stage 1 (M_S2) 1.660 -> 1.775 ms,
+// so M_S2 keeps the separate face phase.
+#ifndef HEVI_X_MERGE_MASK
+#define HEVI_X_MERGE_MASK ((1 << M_R) | (1 << M_L) | (1 << M_S1) | (1 << M_S3) | (1 << M_RK))
+#endif
+
 __device__ __forceinline__ void pf_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -234,7 +243,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                 double d = 0.0;
 #pragma unroll
                 for (int m = 0; m <= N; ++m) d = fma(D.x[m], sx[m], d);
-                if (MAIN) {
+                if (MAIN && !(((HEVI_X_MERGE_MASK >> MODE) & 1) && f == 5)) {
                     // branch-free: the XF slot is in bounds for every main point
                     const double xf = xfp[f * (TX * T::OYM * N) + k];
                     d += ax.face ? xf : 0.0;
@@ -583,13 +592,30 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                                     lt[T_IRT0], lt[T_P0F], bc, a.ph);
             }
         }
+        if ((HEVI_X_MERGE_MASK >> MODE) & 1) {
+            // face partials of the 5 state fields need only the TMA data
+            constexpr int NXF5 = 5 * TX * T::OYM * N;
+            for (int it = tid; it < NXF5; it += BLK) {
+                const int oz = it % N;
+                int t = it / N;
+                const int oy = t % T::OYM;
+                t /= T::OYM;
+                const int ae = t % TX;
+                const int f = t / TX;
+                const double* sx = S + f * PL + ((base + oz) % RING) * SS + (oy + NY) * LXT + ae * N;
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sx[m], s);
+                XF[it] = s;
+            }
+        }
         PH(1);
         __syncthreads();
         PH(2);
         // ---------------- 2. shared partial sums ----------------------------
         double* CARw = CAR + (ez & 1) * (7 * T::CYW * T::CXW);
         const double* CARr = CAR + ((ez + 1) & 1) * (7 * T::CYW * T::CXW);
-        {
+        if (!((HEVI_X_MERGE_MASK >> MODE) & 1)) {
             // row N of the left element at the tile's element x-faces
             constexpr int NXF = T::XF_N;
             for (int it = tid; it < NXF; it += BLK) {
@@ -607,7 +633,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
             }
         }
         PH(3);
-        __syncthreads();
+        if (!((HEVI_X_MERGE_MASK >> MODE) & 1)) __syncthreads();
         PH(4);
         // ---------------- 3. points ------------------------------------------
         if (main_ok) {
