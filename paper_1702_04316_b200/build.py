@@ -25,7 +25,9 @@ def needs_build() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = SRC + [os.path.join(ROOT, "include", "hevi.h")]
+    csrc = os.path.join(HERE, "csrc")
+    deps = SRC + [os.path.join(ROOT, "include", "hevi.h")] + [
+        os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith((".cuh", ".cu", ".h"))]
     return any(os.path.getmtime(s) > t for s in deps)
 
 
