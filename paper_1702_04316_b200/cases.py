@@ -9,7 +9,6 @@ from __future__ import annotations
 
 import math
 
-import numpy as np
 
 
 def bubble_lattice(mesh, ref, theta_c=0.5, centre=None, radii=(250.0, 250.0, 250.0),

@@ -1065,7 +1065,6 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 }
 
 #include "explicit_v2.cuh"
-#include "explicit_v3.cuh"
 #include "explicit_c.cuh"
 #include "solve_v2.cuh"
 #include "imex3d.cuh"
@@ -1108,7 +1107,6 @@ struct hevi_plan {
     int force_pivoted = 0;   // HEVI_OPT_FORCE_PIVOTED (tests of the fallback path)
     unsigned long long* d_dbg = nullptr;
     bool use_v2 = true;
-    bool use_v3 = false;
     bool use_tma = true;
 };
 
@@ -1236,46 +1234,8 @@ int make_tmap(CUtensorMap* m, const Geo& g, const double* base, int bx, int by, 
     return HEVI_OK;
 }
 
-template <int N, int NY>
-struct Tile3 {
-    static constexpr int TX = 0, TY = 0;
-};
-template <> struct Tile3<4, 4> { static constexpr int TX = 4, TY = 2; };
-
-template <int N, int NY, int MODE>
-int launch_e3(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) {
-    constexpr int TX = Tile3<N, NY>::TX, TY = Tile3<N, NY>::TY;
-    done = false;
-    if constexpr (TX == 0 || MODE == M_RK) {
-        return HEVI_OK;
-    } else {
-        using T = E3<N, NY, TX, TY>;
-        const Geo& g = pl->g;
-        const size_t smem = T::fixed_bytes() + sizeof(double) * T::NTAB * g.Z;
-        if (smem > 225 * 1024) return HEVI_OK;
-        auto kern = k_explicit3<N, NY, TX, TY, MODE>;
-        static size_t attr = 0;
-        if (attr < smem) {
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = smem;
-        }
-        CUtensorMap tm;
-        int rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, T::NL);
-        if (rc) return rc;
-        dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
-        kern<<<grid, T::BLK, smem, st>>>(a, tm);
-        CK(cudaGetLastError());
-        done = true;
-        return HEVI_OK;
-    }
-}
-
 template <int N, int NY, int MODE>
 int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) {
-    if (pl->use_v3) {
-        int rc = launch_e3<N, NY, MODE>(pl, a, st, done);
-        if (rc || done) return rc;
-    }
     constexpr int TX = Tile2<N, NY>::TX, TY = Tile2<N, NY>::TY;
     done = false;
     if constexpr (TX == 0) {
@@ -1741,7 +1701,6 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     }
     pl->use_v2 = getenv("HEVI_KERNELS") == nullptr || strcmp(getenv("HEVI_KERNELS"), "v1") != 0;
     pl->use_tma = getenv("HEVI_NO_TMA") == nullptr;
-    pl->use_v3 = getenv("HEVI_KERNELS") != nullptr && strcmp(getenv("HEVI_KERNELS"), "v3") == 0;
     *out = pl;
     return HEVI_OK;
 }

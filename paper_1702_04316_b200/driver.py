@@ -21,7 +21,6 @@ dG and the standard (5-variable) form raise ``NotImplementedError``.
 from __future__ import annotations
 
 import ctypes
-import math
 import os
 import sys
 import time
