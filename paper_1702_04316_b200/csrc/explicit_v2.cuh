@@ -29,6 +29,15 @@
 // one barrier per layer.  Measured at config 5: stage 0 (M_S1) 1.581 -> 1.548
 // ms, stage 2 (M_S3) 1.443 -> 1.402 ms, but stage 1 (M_S2) 1.660 -> 1.775 ms,
 // so M_S2 keeps the separate face phase.
+// The pointwise stage inputs A / F of the layer's owned points arrive by TMA
+// (4D box OX x OYM x N x 5) issued at the start of the layer and are read from
+// shared memory in the epilogue (no registers held through the derivative
+// phase, no exposed global latency); even N only (x origin must be even).
+// Measured at config 5: M_S2 (stage 1) 1.659 -> 1.584 ms; M_S3 (stage 2, F
+// only) 1.402 -> 1.475 ms, so M_S3 keeps its early register loads.
+#ifndef HEVI_X_AFTMA_MASK
+#define HEVI_X_AFTMA_MASK (1 << M_S2)
+#endif
 #ifndef HEVI_X_MERGE_MASK
 #define HEVI_X_MERGE_MASK ((1 << M_R) | (1 << M_L) | (1 << M_S1) | (1 << M_S3) | (1 << M_RK))
 #endif
@@ -66,8 +75,11 @@ struct E2 {
     static constexpr int CAR_N = 2 * 7 * CYW * CXW;           // double-buffered carry
     static constexpr int XF_N = 6 * TX * OYM * N;             // x-face partials
     static constexpr int DN = (N + 1) * (N + 1), DNY = (NY + 1) * (NY + 1);
+    static constexpr int AFB = OX * OYM * N * 5;                 // one A or F layer box
+    static constexpr int AF_N = (HEVI_X_AFTMA_MASK && N % 2 == 0) ? 2 * AFB : 0;
+    static constexpr uint32_t AF_BYTES = (uint32_t)(sizeof(double) * AFB);
     static constexpr size_t fixed_bytes() {
-        return sizeof(double) * (size_t)(S_N + CAR_N + XF_N + DN + DNY + 2) + 128;
+        return sizeof(double) * (size_t)(S_N + AF_N + CAR_N + XF_N + DN + DNY + 3) + 128;
     }
     static constexpr int NTAB = 12;                           // level tables in smem
     static constexpr uint32_t LVL_BYTES = (uint32_t)(sizeof(double) * 5 * PL);   // one level TMA
@@ -162,7 +174,8 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                                        const DRows<N, NY, K>& D, const double* __restrict__ sDx,
                                        const double* __restrict__ sDy, const PAx& ax, const PAx& ay,
                                        int oz0, int ox, int oy, int gx, int gy, int ez, double cx,
-                                       double cy, int Z) {
+                                       double cy, int Z, const double* __restrict__ sAF = nullptr,
+                                       uint64_t* mbaf = nullptr) {
     using T = E2<N, NY, TX, TY>;
     constexpr int PL = T::PL, LXT = T::LXT, RING = T::RING, SS = T::SS;
     constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
@@ -170,6 +183,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
     const Geo& g = a.g;
     const long long fs = g.fs;
     const int base = ez * N;
+    (void)mbaf;
     long long o[K];
     int sl[K], gzk[K];
 #pragma unroll
@@ -179,9 +193,11 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
         sl[k] = (base + oz0 + k) % RING;
     }
     // stage inputs read pointwise: issue early, consume in the epilogue
+    // (MAIN points with a staged A/F box read them from shared memory instead)
     double Ain[K][5], Fin[K][5];
+    const bool af_smem = MAIN && T::AF_N > 0 && sAF != nullptr && ((HEVI_X_AFTMA_MASK >> MODE) & 1);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < K && !af_smem; ++k) {
         if (MODE == M_S2 || (MODE == M_RK && a.A != nullptr)) {
 #pragma unroll
             for (int f = 0; f < 5; ++f) Ain[k][f] = a.A[o[k] + f * fs];
@@ -351,6 +367,17 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
         }
     }
     const double gr = a.ph.g;
+    if (af_smem) {
+        mbar_wait(mbaf, ez & 1);
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                const int i = ((f * N + oz0 + k) * T::OYM + oy) * T::OX + ox;
+                if (MODE == M_S2) Ain[k][f] = sAF[i];
+                Fin[k][f] = sAF[T::AFB + i];
+            }
+    }
     const bool bx = (gx == 0) || (gx == g.X - 1);
     const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
 #pragma unroll
@@ -466,7 +493,8 @@ __device__ __forceinline__ void stage_level_manual(double* slot, const EArgs& a,
 
 template <int N, int NY, int TX, int TY, int MODE, int MINB>
 __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
-    k_explicit2(const EArgs a, const __grid_constant__ CUtensorMap tmap) {
+    k_explicit2(const EArgs a, const __grid_constant__ CUtensorMap tmap,
+                const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmF) {
     using T = E2<N, NY, TX, TY>;
     constexpr int PL = T::PL, LXT = T::LXT, RING = T::RING, SS = T::SS, BLK = T::BLK;
     constexpr bool NEED_R = (MODE != M_L);
@@ -475,12 +503,13 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     double* smd = reinterpret_cast<double*>(
         smraw + ((128u - ((unsigned)__cvta_generic_to_shared(smraw) & 127u)) & 127u));
     double* Sa = smd;                 // ring, 128-byte aligned slots (TMA destinations)
-    double* CAR = Sa + T::S_N;
+    double* sAF = Sa + T::S_N;        // [A | F] layer boxes (128-byte aligned)
+    double* CAR = sAF + T::AF_N;
     double* XF = CAR + T::CAR_N;
     double* sDx = XF + T::XF_N;
     double* sDy = sDx + T::DN;
     double* LT = sDy + T::DNY;
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(LT + T::NTAB * a.g.Z);   // [2], per layer parity
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(LT + T::NTAB * a.g.Z);   // [2] per layer parity, [2] A/F
     const Geo& g = a.g;
     const int Z = g.Z;
     const int tid = threadIdx.x;
@@ -497,6 +526,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     if (tid == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
+        mbar_init(&mbar[2], 1);
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
     }
     for (int i = tid; i < T::DN; i += BLK) sDx[i] = a.Dx[i];
@@ -567,8 +597,21 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
 #else
 #define PH(i) do { } while (0)
 #endif
+    const bool af_tma = T::AF_N > 0 && a.af_tma && ((HEVI_X_AFTMA_MASK >> MODE) & 1);
     for (int ez = 0; ez < g.nez; ++ez) {
         const int base = ez * N;
+        if (af_tma && tid == 0) {
+            // the previous layer's epilogue reads are ordered by its final barrier
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const int ax0 = ex0 * N - g.x0, ay0 = ey0 * NY - g.y0;
+            if (MODE == M_S2) {
+                mbar_expect_tx(&mbar[2], 2 * T::AF_BYTES);
+                tma_load_4d(sAF, &tmA, &mbar[2], ax0, ay0, base, 0);
+            } else {
+                mbar_expect_tx(&mbar[2], T::AF_BYTES);
+            }
+            tma_load_4d(sAF + T::AFB, &tmF, &mbar[2], ax0, ay0, base, 0);
+        }
         // ---------------- 1. this layer's new levels, P' in place -----------
         const int lz0 = (ez == 0) ? 0 : 1;
         if (use_tma) {
@@ -638,7 +681,8 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
         // ---------------- 3. points ------------------------------------------
         if (main_ok) {
             e2_pts<N, NY, TX, TY, MODE, true, K>(a, S, CARr, CARw, XF, LT, Dm, sDx, sDy, max_, may_,
-                                                 moz, mox, moy, mgx, mgy, ez, mcx, mcy, Z);
+                                                 moz, mox, moy, mgx, mgy, ez, mcx, mcy, Z,
+                                                 af_tma ? sAF : nullptr, &mbar[2]);
         }
         // points outside the main box: domain-end x column / y row, top level
         const int ozn = N + ((ez == g.nez - 1) ? 1 : 0);

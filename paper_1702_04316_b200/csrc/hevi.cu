@@ -111,6 +111,7 @@ struct EArgs {
     double bc[16];   // binomial coefficients C(gamma, k), k = 1..15 (EOS series)
     int use_tma;     // 1: TMA staging (default); 0: cooperative loads
     int rk_final;    // M_RK: last stage (non-finite output check, imexcore.py:124-125)
+    int af_tma;      // explicit_v2 M_S2/M_S3: A/F layer boxes by TMA (set by launch_e2)
     unsigned long long* dbg;   // HEVI_PHASE_TIMING builds: per-phase clock64 sums
 };
 
@@ -1254,8 +1255,21 @@ int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) 
         CUtensorMap tm;
         int rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, 1);   // one level per TMA
         if (rc) return rc;
+        EArgs a2 = a;
+        a2.af_tma = 0;
+        CUtensorMap tA = tm, tF = tm;
+        if (T::AF_N > 0 && ((HEVI_X_AFTMA_MASK >> MODE) & 1) && (MODE == M_S2 || MODE == M_S3) && a.F &&
+            (MODE == M_S3 || a.A) && (g.x0 % 2 == 0)) {
+            if (MODE == M_S2) {
+                rc = make_tmap(&tA, g, a.A, T::OX, T::OYM, N);
+                if (rc) return rc;
+            }
+            rc = make_tmap(&tF, g, a.F, T::OX, T::OYM, N);
+            if (rc) return rc;
+            a2.af_tma = 1;
+        }
         dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
-        kern<<<grid, T::BLK, smem, st>>>(a, tm);
+        kern<<<grid, T::BLK, smem, st>>>(a2, tm, tA, tF);
         CK(cudaGetLastError());
         done = true;
         return HEVI_OK;
