@@ -24,11 +24,6 @@
 //      L_V(q) pointwise, no-flux projection, fused ARK2 stage epilogue.
 #pragma once
 
-// Per mode (bit MODE): form the x-face partials of the 5 state fields in the
-// P' phase and let the face points take their own P' face line, which drops
-// one barrier per layer.  Measured at config 5: stage 0 (M_S1) 1.581 -> 1.548
-// ms, stage 2 (M_S3) 1.443 -> 1.402 ms, but stage 1 (M_S2) 1.660 -> 1.775 ms,
-// so M_S2 keeps the separate face phase.
 // The pointwise stage inputs A / F of the layer's owned points arrive by TMA
 // (4D box OX x OYM x N x 5) issued at the start of the layer and are read from
 // shared memory in the epilogue (no registers held through the derivative
@@ -38,8 +33,13 @@
 #ifndef HEVI_X_AFTMA_MASK
 #define HEVI_X_AFTMA_MASK (1 << M_S2)
 #endif
+// Per mode (bit MODE): form the x-face partials of the 5 state fields in the
+// P' phase and let the face points take their own P' face line, which drops
+// one barrier per layer.  Measured at config 5: stage 0 (M_S1) 1.581 -> 1.548
+// ms, stage 2 (M_S3) 1.443 -> 1.402 ms, stage 1 (M_S2, with its A/F boxes
+// staged by TMA) 1.584 -> 1.537 ms (before the A/F staging it was slower).
 #ifndef HEVI_X_MERGE_MASK
-#define HEVI_X_MERGE_MASK ((1 << M_R) | (1 << M_L) | (1 << M_S1) | (1 << M_S3) | (1 << M_RK))
+#define HEVI_X_MERGE_MASK 63
 #endif
 
 __device__ __forceinline__ void pf_l2(const void* p) {
@@ -78,8 +78,11 @@ struct E2 {
     static constexpr int AFB = OX * OYM * N * 5;                 // one A or F layer box
     static constexpr int AF_N = (HEVI_X_AFTMA_MASK && N % 2 == 0) ? 2 * AFB : 0;
     static constexpr uint32_t AF_BYTES = (uint32_t)(sizeof(double) * AFB);
-    static constexpr size_t fixed_bytes() {
-        return sizeof(double) * (size_t)(S_N + AF_N + CAR_N + XF_N + DN + DNY + 3) + 128;
+    // shared bytes of a mode (the A/F boxes only where that mode stages them)
+    __host__ __device__ static constexpr int af_of(int mode) { return ((HEVI_X_AFTMA_MASK >> mode) & 1) ? AF_N : 0; }
+    static constexpr size_t fixed_bytes(int mode = -1) {
+        return sizeof(double) * (size_t)(S_N + (mode < 0 ? AF_N : af_of(mode)) + CAR_N + XF_N + DN +
+                                         DNY + 3) + 128;
     }
     static constexpr int NTAB = 12;                           // level tables in smem
     static constexpr uint32_t LVL_BYTES = (uint32_t)(sizeof(double) * 5 * PL);   // one level TMA
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
         smraw + ((128u - ((unsigned)__cvta_generic_to_shared(smraw) & 127u)) & 127u));
     double* Sa = smd;                 // ring, 128-byte aligned slots (TMA destinations)
     double* sAF = Sa + T::S_N;        // [A | F] layer boxes (128-byte aligned)
-    double* CAR = sAF + T::AF_N;
+    double* CAR = sAF + T::af_of(MODE);
     double* XF = CAR + T::CAR_N;
     double* sDx = XF + T::XF_N;
     double* sDy = sDx + T::DN;

@@ -1244,7 +1244,7 @@ int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) 
     } else {
         using T = E2<N, NY, TX, TY>;
         const Geo& g = pl->g;
-        const size_t smem = T::fixed_bytes() + sizeof(double) * T::NTAB * g.Z;
+        const size_t smem = T::fixed_bytes(MODE) + sizeof(double) * T::NTAB * g.Z;
         if (smem > 225 * 1024) return HEVI_OK;   // v1 handles it
         auto kern = k_explicit2<N, NY, TX, TY, MODE, Tile2<N, NY>::MINB>;
         static size_t attr = 0;
