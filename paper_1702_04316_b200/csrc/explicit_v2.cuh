@@ -42,6 +42,28 @@
 #define HEVI_X_MERGE_MASK 63
 #endif
 
+#ifndef HEVI_X_TREE
+#define HEVI_X_TREE 0   // 1: line sums as two interleaved chains (depth ~N/2 + 1)
+#endif
+// sum_m D[m] s[m*STR], m = 0..NN: one chain (reference order) or two
+// interleaved chains joined at the end (shorter dependency path)
+template <int NN, int STR>
+__device__ __forceinline__ double line_sum(const double* D, const double* s) {
+    if (HEVI_X_TREE && NN >= 3) {
+        double a = D[0] * s[0], b = D[1] * s[STR];
+#pragma unroll
+        for (int m = 2; m <= NN; m += 2) {
+            a = fma(D[m], s[m * STR], a);
+            if (m + 1 <= NN) b = fma(D[m + 1], s[(m + 1) * STR], b);
+        }
+        return a + b;
+    }
+    double d = 0.0;
+#pragma unroll
+    for (int m = 0; m <= NN; ++m) d = fma(D[m], s[m * STR], d);
+    return d;
+}
+
 __device__ __forceinline__ void pf_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -259,9 +281,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const double* sx = bx_[k] + f * SF;
-                double d = 0.0;
-#pragma unroll
-                for (int m = 0; m <= N; ++m) d = fma(D.x[m], sx[m], d);
+                double d = line_sum<N, 1>(D.x, sx);
                 if (MAIN && !(((HEVI_X_MERGE_MASK >> MODE) & 1) && f == 5)) {
                     // branch-free: the XF slot is in bounds for every main point
                     const double xf = xfp[f * (TX * T::OYM * N) + k];
@@ -277,9 +297,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                 }
                 gxv[k] = cx * d;
                 const double* sy = by_[k] + f * SF;
-                double e = 0.0;
-#pragma unroll
-                for (int m = 0; m <= NY; ++m) e = fma(D.y[m], sy[m * LXT], e);
+                double e = line_sum<NY, LXT>(D.y, sy);
                 if (ay.face) {
                     const double* syl = byl_[k] + f * SF;
                     double h = 0.0;
@@ -302,9 +320,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            double d = 0.0;
-#pragma unroll
-            for (int m = 0; m <= N; ++m) d = fma(D.z[k][m], val[m], d);
+            double d = line_sum<N, 1>(D.z[k], val);
             if (k == 0) {
                 const double cr = carp[f * (T::CYW * T::CXW)];
                 d += zface ? cr : 0.0;
