@@ -155,6 +155,13 @@ int hevi_wdot(const hevi_plan *plan, const double *x, const double *y, int nf, d
               void *stream);
 int hevi_axpby(long long n, double alpha, const double *x, double beta, double *y, void *stream);
 
+/* Direct solve of the standard 5-variable form (columnsolve.solve_direct with
+ * form = "standard", columnsolve.py:196-204) on lattice arrays of this plan:
+ * q = (I - lam L_V)^-1 q_e column by column with one shared band LU factor
+ * (band storage of hevi_band_pack with n_col = 1, M = 5 Z, unknown lev*5 + field). */
+int hevi_std_solve(const hevi_plan *plan, const double *band, int M, int nb, const double *qe,
+                   double *q, void *stream);
+
 /* Run diagnostics (bench.total_mass / max_perturbations, bench.py:131-137) of a
  * lattice state of this plan: out_host[0] = sum_g Wx[gx] Wy[gy] Wz[gz] (rho0 +
  * rho'), out_host[1] = max |rho'|, out_host[2] = max |q4|; Wx/Wy/Wz are the

@@ -71,6 +71,7 @@ SIGNATURES = {
     "hevi_absmax": (_I, [_V, _LL, ctypes.POINTER(_D), _V]),
     "hevi_lu_pivot": (_I, [_V, _V, _I, _I, _V, _V]),
     "hevi_diagnostics": (_I, [_V, _V, _V, _V, _V, _V, _V]),
+    "hevi_std_solve": (_I, [_V, _V, _I, _I, _V, _V, _V]),
     "hevi_linear3": (_I, [_V, _V, _V, _V]),
     "hevi_schur3_up": (_I, [_V, _D, _I, _V, _V, _V]),
     "hevi_schur3_flux": (_I, [_V, _D, _I, _V, _V, _V, _V]),

@@ -213,8 +213,62 @@ def get_factors(problem) -> ColumnJacobian:
     return problem._column_cache[key]
 
 
+def standard_column_factor(problem):
+    """Shared band LU of the standard-form column operator I - lam L_V
+    (M = 5 n_lev unknowns, unknown lev*5 + field; half band 5N+3, SURVEY
+    8(a) a17), cached per (round(lam, 12), "standard") like get_factors.
+    Probed as the reference does (columnsolve.py:75-108): one device
+    application of L_V per unknown with the unit vector in every column (box
+    columns are identical), the response of one interior column assembled."""
+    import torch
+    key = (round(problem.lam, 12), "standard")
+    if key in problem._column_cache:
+        return problem._column_cache[key]
+    plan = problem.disc.plan_for(problem.ref, problem.set_name)
+    mesh = problem.disc.mesh
+    lam = float(problem.lam)
+    Z, X = mesh.Z, mesh.X
+    M = 5 * Z
+    gx, gy = X // 2, (0 if mesh.slab else mesh.Y // 2)
+    U, out = plan.zeros(), plan.zeros()
+    A = np.zeros((M, M))
+    for lev in range(Z):
+        for d in range(5):
+            U.zero_()
+            U[d, lev, :, :X] = 1.0
+            plan.linear(U, out)
+            plan.axpby(1.0, U, -lam, out)                 # U - lam L_V(U)
+            A[:, lev * 5 + d] = out[:, :, gy, gx].T.reshape(-1).cpu().numpy()
+    plan.check_flags()
+    scale = np.abs(A).max()
+    rows, cols = np.nonzero(np.abs(A) > 1e-14 * scale)
+    nb = int(np.abs(rows - cols).max()) + 1 if len(rows) else 1
+    lib = nv.load()
+    At = torch.as_tensor(A[None], device=plan.device).contiguous()
+    band = torch.empty((2 * nb - 1, M, 1), dtype=torch.float64, device=plan.device)
+    s = nv.stream_ptr()
+    nv.check(lib.hevi_band_pack(nv.ptr(At), nv.ptr(band), 1, M, nb, s))
+    bad = ctypes.c_int(-1)
+    nv.check(lib.hevi_band_lu(nv.ptr(band), 1, M, nb, float(scale), ctypes.byref(bad), s))
+    if bad.value >= 0:
+        raise RuntimeError("no-pivot LU of the standard-form column hit a degenerate diagonal")
+    ent = (A, band, nb)
+    problem._column_cache[key] = ent
+    return ent
+
+
 def solve_direct(problem, q_e):
     """One direct implicit solve (columnsolve.py:191-210): the fused device
-    column kernel with the shared per-lam factor."""
+    column kernel with the shared per-lam factor (Schur form), or the
+    standard-form column substitution on the lattice."""
     plan = problem.disc.plan_for(problem.ref, problem.set_name)
+    if problem.form == "standard":
+        from .plan import to_device
+        _, band, nb = standard_column_factor(problem)
+        E, back = to_device(q_e)
+        Qe = plan.e2l(E)
+        q = plan.zeros()
+        nv.check(plan.lib.hevi_std_solve(plan.h, nv.ptr(band), 5 * plan.Z, nb, nv.ptr(Qe), nv.ptr(q),
+                                         nv.stream_ptr()))
+        return back(plan.l2e(q))
     return plan.apply_evec("solve", q_e, lam=float(problem.lam))

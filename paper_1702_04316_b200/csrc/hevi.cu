@@ -1056,6 +1056,39 @@ __global__ void k_band_solve(const double* B, double* rhs, int n_col, int M, int
     }
 }
 
+// Direct solve of the standard (5-variable) form, one thread per column
+// (columnsolve.solve_direct, form="standard", columnsolve.py:196-204): the
+// unknown i = lev*5 + field of a column is read straight from the lattice
+// (coalesced across columns), one shared band LU (box columns are identical),
+// forward / backward substitution in place in the output lattice.
+__global__ void k_std_solve(const Geo g, int N, const double* __restrict__ B, int M, int nb,
+                            const double* __restrict__ qe, double* __restrict__ q) {
+    extern __shared__ double sB[];
+    const int W = 2 * nb - 1;
+    for (int i = threadIdx.x; i < W * M; i += blockDim.x) sB[i] = B[i];
+    __syncthreads();
+    const int NYo = g.slab ? 1 : N;
+    const int cntx = (g.ex_e - g.ex_b) * N + (g.ex_e == g.nex ? 1 : 0);
+    const int cnty = (g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cntx * cnty) return;
+    const int gx = g.ex_b * N + c % cntx, gy = g.ey_b * NYo + c / cntx;
+    const long long col = loff(g, gx, gy, 0);
+    const long long ls = (long long)g.lY * g.px;
+    auto at = [&](int i) { return (long long)(i % 5) * g.fs + (long long)(i / 5) * ls + col; };
+    const int o = nb - 1;
+    for (int i = 0; i < M; ++i) {
+        double s = 0.0;
+        for (int j = max(0, i - nb + 1); j < i; ++j) s = fma(sB[(j - i + o) * M + i], q[at(j)], s);
+        q[at(i)] = qe[at(i)] - s;
+    }
+    for (int i = M - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int j = i + 1; j < min(i + nb, M); ++j) s = fma(sB[(j - i + o) * M + i], q[at(j)], s);
+        q[at(i)] = (q[at(i)] - s) / sB[o * M + i];
+    }
+}
+
 __global__ void k_absmax(const double* a, long long n, unsigned long long* out) {
     double m = 0.0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -2179,6 +2212,21 @@ int hevi_diagnostics(const hevi_plan* pl, const double* q, const double* wx, con
     CK(cudaMemcpyAsync(out_host, d + 3 * DIAG_BLOCKS, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaFreeAsync(d, st));
     CK(cudaStreamSynchronize(st));
+    return HEVI_OK;
+}
+
+int hevi_std_solve(const hevi_plan* pl, const double* band, int M, int nb, const double* qe, double* q,
+                   void* stream) {
+    if (!pl || !band || !qe || !q || nb < 1 || M != 5 * pl->g.Z) return fail("bad std_solve arguments");
+    const Geo& g = pl->g;
+    const size_t smem = sizeof(double) * (size_t)(2 * nb - 1) * M;
+    if (smem > 225 * 1024) return fail("standard-form band too wide for the column kernel");
+    CK(cudaFuncSetAttribute(k_std_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int NYo = g.slab ? 1 : pl->N;
+    const long long nc = ((long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0)) *
+                         ((long long)(g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0));
+    k_std_solve<<<(int)((nc + 127) / 128), 128, smem, (cudaStream_t)stream>>>(g, pl->N, band, M, nb, qe, q);
+    CK(cudaGetLastError());
     return HEVI_OK;
 }
 

@@ -178,8 +178,8 @@ class ImplicitProblem:
                                       "use SolverSpec(method='direct') with dim='1d'")
         if self.dim != "1d":
             raise ValueError("the direct column solver requires the 1D form")
-        if self.form != "schur":
-            raise NotImplementedError("the device path implements the Schur (pressure) form")
+        if self.form not in ("schur", "standard"):
+            raise ValueError(f"unknown form {self.form!r}")
         euler._check_set(self.set_name)
 
     @property
@@ -188,7 +188,7 @@ class ImplicitProblem:
             self._check_path()
         except (NotImplementedError, ValueError):
             return False
-        return True
+        return self.form == "schur"
 
     def linear(self, q):
         """imexcore.py:190-194."""

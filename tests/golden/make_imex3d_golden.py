@@ -2,7 +2,7 @@
 dim="3d", form="schur", Krylov solvers + PBNO; SURVEY 8(d) config 4 /
 8(f) rank 1), made by the UNMODIFIED reference:
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_imex3d_golden.py [--1d | --standard]
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_imex3d_golden.py [--1d | --standard | --direct-standard]
 
 Per case (isotropic 3D box, 3x3x3 elements, N=4, both equation sets):
 full linear operator L(q), Schur rhs, lhs_schur(P), Krylov solves
@@ -70,7 +70,7 @@ def run(name, set_name, lam=0.4, C=4.0, nsteps=3):
     print(name, "dt", dt, {k: int(v) for k, v in out.items() if k.startswith(("iters", "step_it"))})
 
 
-if __name__ == "__main__" and "--1d" not in sys.argv and "--standard" not in sys.argv:
+if __name__ == "__main__" and not set(sys.argv) & {"--1d", "--standard", "--direct-standard"}:
     run("imex3d_box", "set2nc")
     run("imex3d_box_c", "set2c")
 
@@ -142,3 +142,41 @@ def run_standard(name="krylov_standard"):
 
 if __name__ == "__main__" and "--standard" in sys.argv:
     run_standard()
+
+
+def run_standard_direct(name="direct_standard"):
+    """Direct (column LU) solves of the standard 5-variable form (dim='1d',
+    columnsolve.py:196-204) and the probed column matrix."""
+    from make_golden import sg, cs
+    out = {}
+    mesh = sg.build_box_mesh(5, 4, 20_000.0, 1000.0, 4)
+    mesh.meta["ny"] = 1
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rep, dims, _ = lattice_index(mesh, 1)
+    qr = continuous_random_state(disc, ref, 32, slab=True)
+    out["slab_q"] = to_lattice(qr, rep, dims)
+    p = imx.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="standard", dim="1d",
+                            solver=imx.SolverSpec(method="direct"))
+    p.lam = 0.8
+    out["slab_solve"] = to_lattice(p.solve(qr), rep, dims)
+    cj = cs.build_column_jacobian(p)
+    out["slab_A0"] = cj.matrices[0]
+    out["slab_nb"] = np.array(cj.bandwidth)
+    mesh = box3d_mesh(3, 3, 3, 12_000.0, 12_000.0, 300.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    rep, dims, _ = lattice_index(mesh, 4)
+    qr = continuous_random_state(disc, ref, 22, slab=False)
+    out["box_q"] = to_lattice(qr, rep, dims)
+    for sn in ("set2nc", "set2c"):
+        p = imx.ImplicitProblem(disc=disc, ref=ref, set_name=sn, form="standard", dim="1d",
+                                solver=imx.SolverSpec(method="direct"))
+        p.lam = 0.3
+        out[f"box_{sn}"] = to_lattice(p.solve(qr), rep, dims)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "nb", int(out["slab_nb"]))
+
+
+if __name__ == "__main__" and "--direct-standard" in sys.argv:
+    run_standard_direct()
