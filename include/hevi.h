@@ -162,6 +162,15 @@ int hevi_axpby(long long n, double alpha, const double *x, double beta, double *
 int hevi_std_solve(const hevi_plan *plan, const double *band, int M, int nb, const double *qe,
                    double *q, void *stream);
 
+/* Halo exchange of the column-partitioned step (SURVEY 8(b) "halo_pack"): copy
+ * the region [xlo, xhi) x [ylo, yhi) (global lattice indices, all levels, nf
+ * fields) of a lattice array of this plan into / out of a contiguous
+ * (nf, Z, yhi-ylo, xhi-xlo) buffer for one NCCL send / recv per neighbour. */
+int hevi_halo_pack(const hevi_plan *plan, const double *q, int nf, int xlo, int xhi, int ylo,
+                   int yhi, double *buf, void *stream);
+int hevi_halo_unpack(const hevi_plan *plan, double *q, int nf, int xlo, int xhi, int ylo, int yhi,
+                     const double *buf, void *stream);
+
 /* Run diagnostics (bench.total_mass / max_perturbations, bench.py:131-137) of a
  * lattice state of this plan: out_host[0] = sum_g Wx[gx] Wy[gy] Wz[gz] (rho0 +
  * rho'), out_host[1] = max |rho'|, out_host[2] = max |q4|; Wx/Wy/Wz are the

@@ -72,6 +72,8 @@ SIGNATURES = {
     "hevi_lu_pivot": (_I, [_V, _V, _I, _I, _V, _V]),
     "hevi_diagnostics": (_I, [_V, _V, _V, _V, _V, _V, _V]),
     "hevi_std_solve": (_I, [_V, _V, _I, _I, _V, _V, _V]),
+    "hevi_halo_pack": (_I, [_V, _V, _I, _I, _I, _I, _I, _V, _V]),
+    "hevi_halo_unpack": (_I, [_V, _V, _I, _I, _I, _I, _I, _V, _V]),
     "hevi_linear3": (_I, [_V, _V, _V, _V]),
     "hevi_schur3_up": (_I, [_V, _D, _I, _V, _V, _V]),
     "hevi_schur3_flux": (_I, [_V, _D, _I, _V, _V, _V, _V]),

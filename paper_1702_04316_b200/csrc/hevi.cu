@@ -1089,6 +1089,30 @@ __global__ void k_std_solve(const Geo g, int N, const double* __restrict__ B, in
     }
 }
 
+// Halo pack / unpack for the column-partitioned step (SURVEY 8(b)
+// "halo_pack"): a region [xlo, xhi) x [ylo, yhi) (global lattice indices) of
+// every level and nf fields <-> a contiguous (nf, Z, ny, nx) buffer, so one
+// NCCL send/recv per neighbour moves it.
+__global__ void k_halo(const Geo g, double* q, int nf, int xlo, int xhi, int ylo, int yhi,
+                       double* buf, int unpack) {
+    const int nx = xhi - xlo, ny = yhi - ylo;
+    const long long n = (long long)nf * g.Z * ny * nx;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx);
+        long long t = i / nx;
+        const int y = (int)(t % ny);
+        t /= ny;
+        const int z = (int)(t % g.Z);
+        const int f = (int)(t / g.Z);
+        const long long o = f * g.fs + loff(g, xlo + x, ylo + y, z);
+        if (unpack)
+            q[o] = buf[i];
+        else
+            buf[i] = q[o];
+    }
+}
+
 __global__ void k_absmax(const double* a, long long n, unsigned long long* out) {
     double m = 0.0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -2228,6 +2252,28 @@ int hevi_std_solve(const hevi_plan* pl, const double* band, int M, int nb, const
     k_std_solve<<<(int)((nc + 127) / 128), 128, smem, (cudaStream_t)stream>>>(g, pl->N, band, M, nb, qe, q);
     CK(cudaGetLastError());
     return HEVI_OK;
+}
+
+static int halo_call(const hevi_plan* pl, double* q, int nf, int xlo, int xhi, int ylo, int yhi,
+                     double* buf, int unpack, void* stream) {
+    if (!pl || !q || !buf || nf < 1) return fail("null argument");
+    const Geo& g = pl->g;
+    if (xlo < g.x0 || xhi > g.x0 + g.lX || ylo < g.y0 || yhi > g.y0 + g.lY || xlo >= xhi || ylo >= yhi)
+        return fail("halo region outside the plan's window");
+    const long long n = (long long)nf * g.Z * (yhi - ylo) * (xhi - xlo);
+    k_halo<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(g, q, nf, xlo, xhi, ylo, yhi, buf, unpack);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_halo_pack(const hevi_plan* pl, const double* q, int nf, int xlo, int xhi, int ylo, int yhi,
+                   double* buf, void* stream) {
+    return halo_call(pl, const_cast<double*>(q), nf, xlo, xhi, ylo, yhi, buf, 0, stream);
+}
+
+int hevi_halo_unpack(const hevi_plan* pl, double* q, int nf, int xlo, int xhi, int ylo, int yhi,
+                     const double* buf, void* stream) {
+    return halo_call(pl, q, nf, xlo, xhi, ylo, yhi, const_cast<double*>(buf), 1, stream);
 }
 
 int hevi_absmax(const double* a, long long n, double* out_host, void* stream) {

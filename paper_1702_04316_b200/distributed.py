@@ -102,31 +102,75 @@ def _view(t, region, w):
     return t[:, :, ylo - w["y0"]:yhi - w["y0"], xlo - w["x0"]:xhi - w["x0"]]
 
 
-class HaloExchange:
-    """Grouped point-to-point halo refresh over torch.distributed."""
+def pack(plan, t, region, buf=None):
+    """Region (global lattice indices) of a CUDA lattice tensor -> contiguous
+    (nf, Z, ny, nx) buffer by the ``hevi_halo_pack`` kernel."""
+    import torch
+    from . import _native as nv
+    xlo, xhi, ylo, yhi = region
+    nf = t.shape[0]
+    if buf is None:
+        buf = torch.empty((nf, t.shape[1], yhi - ylo, xhi - xlo), dtype=t.dtype, device=t.device)
+    nv.check(plan.lib.hevi_halo_pack(plan.h, nv.ptr(t), nf, xlo, xhi, ylo, yhi, nv.ptr(buf),
+                                     nv.stream_ptr()))
+    return buf
 
-    def __init__(self, mesh, px, py, rank, group=None):
+
+def unpack(plan, t, region, buf):
+    """Contiguous buffer -> region of a CUDA lattice tensor (``hevi_halo_unpack``)."""
+    from . import _native as nv
+    xlo, xhi, ylo, yhi = region
+    nv.check(plan.lib.hevi_halo_unpack(plan.h, nv.ptr(t), t.shape[0], xlo, xhi, ylo, yhi,
+                                       nv.ptr(buf), nv.stream_ptr()))
+
+
+class HaloExchange:
+    """Grouped point-to-point halo refresh over torch.distributed.  With a
+    plan and CUDA tensors the regions are packed / unpacked by the library's
+    halo kernels into reused contiguous buffers (one NCCL send and receive per
+    neighbour and phase); CPU tensors (gloo tests) use strided copies."""
+
+    def __init__(self, mesh, px, py, rank, group=None, plan=None):
         self.block, self.phases = halo_plan(mesh, px, py, rank)
         self.group = group
+        self.plan = plan
+        self._bufs = {}
+
+    def _buf(self, key, shape, like):
+        import torch
+        b = self._bufs.get(key)
+        if b is None or tuple(b.shape) != tuple(shape):
+            b = torch.empty(shape, dtype=like.dtype, device=like.device)
+            self._bufs[key] = b
+        return b
 
     def __call__(self, t):
         import torch
         import torch.distributed as dist
         w = self.block.window
-        for phase in self.phases:
+        native = self.plan is not None and t.is_cuda
+        for ip, phase in enumerate(self.phases):
             if not phase:
                 continue
             ops, recvs = [], []
             for peer, sreg, rreg in phase:
-                sbuf = _view(t, sreg, w).contiguous()
-                rbuf = torch.empty_like(_view(t, rreg, w))
+                if native:
+                    shp = lambda r: (t.shape[0], t.shape[1], r[3] - r[2], r[1] - r[0])  # noqa: E731
+                    sbuf = pack(self.plan, t, sreg, self._buf(("s", ip, peer), shp(sreg), t))
+                    rbuf = self._buf(("r", ip, peer), shp(rreg), t)
+                else:
+                    sbuf = _view(t, sreg, w).contiguous()
+                    rbuf = torch.empty_like(_view(t, rreg, w))
                 ops.append(dist.P2POp(dist.isend, sbuf, peer, group=self.group))
                 ops.append(dist.P2POp(dist.irecv, rbuf, peer, group=self.group))
                 recvs.append((rreg, rbuf))
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
             for rreg, rbuf in recvs:
-                _view(t, rreg, w).copy_(rbuf)
+                if native:
+                    unpack(self.plan, t, rreg, rbuf)
+                else:
+                    _view(t, rreg, w).copy_(rbuf)
 
 
 class DistributedStepper:
@@ -136,7 +180,8 @@ class DistributedStepper:
                  set_name="set2nc"):
         self.block = make_block(mesh, px, py, rank)
         self.plan = HeviPlan(mesh, ref, disc, window=self.block.window, set_name=set_name)
-        self.exchange = exchange if exchange is not None else HaloExchange(mesh, px, py, rank)
+        self.exchange = (exchange if exchange is not None
+                         else HaloExchange(mesh, px, py, rank, plan=self.plan))
         self.tableau = tableau or imexcore.ark2_tableau()
         self.tab = tableau_array(self.tableau)
         self.dt = float(dt)
@@ -188,21 +233,29 @@ class LocalExchange:
     check that the partitioned step is bitwise the single-GPU step without
     running ranks that wait on one another)."""
 
-    def __init__(self, mesh, px, py):
+    def __init__(self, mesh, px, py, plans=None):
         self.mesh, self.px, self.py = mesh, px, py
-        self.steppers = None
+        self.plans = plans
 
     def fill(self, rank, t_by_rank):
+        """Phase by phase, as HaloExchange: the sender's halo kernel packs the
+        region out of its window, the receiver's unpacks it into its own."""
         me, phases = halo_plan(self.mesh, self.px, self.py, rank)
         w = me.window
         for phase in phases:
             for peer, sreg, rreg in phase:
-                pw = make_block(self.mesh, self.px, self.py, peer).window
-                _view(t_by_rank[rank], rreg, w).copy_(_view(t_by_rank[peer], rreg, pw))
+                if self.plans is not None and t_by_rank[rank].is_cuda:
+                    buf = pack(self.plans[peer], t_by_rank[peer], rreg)
+                    unpack(self.plans[rank], t_by_rank[rank], rreg, buf)
+                else:
+                    pw = make_block(self.mesh, self.px, self.py, peer).window
+                    _view(t_by_rank[rank], rreg, w).copy_(_view(t_by_rank[peer], rreg, pw))
 
 
 def run_local_partitioned(steppers, exchange: LocalExchange, nsteps=1):
     """Advance all emulated ranks in lock-step on one device."""
+    if exchange.plans is None:
+        exchange.plans = [s.plan for s in steppers]
     for _ in range(nsteps):
         gens = [s.step_stages() for s in steppers]
         while True:

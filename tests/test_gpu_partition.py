@@ -94,3 +94,24 @@ def test_partitioned_set2c_step_is_bitwise_single_gpu(setup, world):
         s.plan.check_flags()
         x0, x1, y0, y1 = s.owned_region()
         assert torch.equal(s.owned()[..., :x1 - x0], want[:, :, y0:y1, x0:x1]), (world, s.block.rank)
+
+
+def test_halo_pack_unpack_kernels_match_strided_copies(setup):
+    """hevi_halo_pack / unpack move exactly the region torch slicing selects."""
+    mesh, ref, disc, q0, dt = setup
+    px, py = dd.grid_for(4)
+    s = dd.DistributedStepper(mesh, ref, disc, dt, px, py, 3)
+    s.load_global(q0)
+    w = s.block.window
+    _, phases = dd.halo_plan(mesh, px, py, 3)
+    for phase in phases:
+        for peer, sreg, rreg in phase:
+            buf = dd.pack(s.plan, s.Q, sreg)
+            assert torch.equal(buf, dd._view(s.Q, sreg, w).contiguous())
+            t = s.Q.clone()
+            src = torch.randn_like(dd._view(t, rreg, w).contiguous())
+            dd.unpack(s.plan, t, rreg, src)
+            assert torch.equal(dd._view(t, rreg, w), src)
+            mask = torch.ones_like(t, dtype=torch.bool)
+            dd._view(mask, rreg, w).fill_(False)
+            assert torch.equal(t[mask], s.Q[mask])        # nothing outside the region moved
