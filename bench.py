@@ -50,15 +50,17 @@ CONFIGS = {
 }
 
 # algorithmic HBM bytes per unique point, per launch: each field
-# read / written once; 8 B per fp64 value
+# read / written once; 8 B per fp64 value.  The column solves also write P' of
+# their output (one plane), which explicit stages 1 and 2 read instead of
+# forming it from rho', theta' for every staged (halo-overlapped) point.
 KERNEL_BYTES_PER_POINT = {
     "explicit_stage0": 8 * (5 + 15),
-    "solve_stage0": 8 * (3 + 3),
-    "explicit_stage1": 8 * (15 + 10),
-    "solve_stage1": 8 * (3 + 3),
-    "explicit_stage2": 8 * (10 + 5),
+    "solve_stage0": 8 * (3 + 3 + 1),
+    "explicit_stage1": 8 * (15 + 1 + 10),
+    "solve_stage1": 8 * (3 + 3 + 1),
+    "explicit_stage2": 8 * (10 + 1 + 5),
 }
-STEP_BYTES_PER_POINT = sum(KERNEL_BYTES_PER_POINT.values())   # 576 B
+STEP_BYTES_PER_POINT = sum(KERNEL_BYTES_PER_POINT.values())   # 608 B
 SURVEY_BYTES_PER_POINT = 640                                   # SURVEY 8(d) 16 state passes
 
 
@@ -247,7 +249,12 @@ def run_gpu(args):
         px, py = grid_for(world)
         ds = DistributedStepper(mesh, ref, disc, dt, px, py, rank, set_name=sn)
         ds.load_global(q0)
-        plan, Q, work, exch = ds.plan, ds.Q, ds.work, ds.exchange
+        plan, Q, work = ds.plan, ds.Q, ds.work
+
+        def exch(s):
+            """halo refresh of everything stage s reads (state [+ P' plane])"""
+            for t in ds.stage_inputs(s):
+                ds.exchange(t)
     del q0
     tarr = tableau_array(tab)
     stream = torch.cuda.current_stream()
@@ -262,7 +269,7 @@ def run_gpu(args):
             plan.rk35(dt, Q, work)
             return
         if exch is not None:
-            exch(Q)
+            exch(0)
         if ev is not None:
             ev[0].record(stream)
         plan.stage(0, dt, tarr, Q, work)
@@ -272,7 +279,7 @@ def run_gpu(args):
         if ev is not None:
             ev[2].record(stream)
         if exch is not None:
-            exch(work[0])
+            exch(1)
             if ev is not None:
                 ev[6].record(stream)
         else:
@@ -285,7 +292,7 @@ def run_gpu(args):
         if ev is not None:
             ev[4].record(stream)
         if exch is not None:
-            exch(work[1])
+            exch(2)
             if ev is not None:
                 ev[7].record(stream)
         else:
@@ -447,13 +454,13 @@ def run_e2e(args, mesh, ref, disc, dt, tab, plan, Q, work, exch, world, rank, do
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         Q.copy_(hin, non_blocking=True)
-        exch(Q)
+        exch(0)
         plan.stage(0, dt, tarr, Q, work)
         plan.stage_solve(0, lam, work)
-        exch(work[0])
+        exch(1)
         plan.stage(1, dt, tarr, Q, work)
         plan.stage_solve(1, lam, work)
-        exch(work[1])
+        exch(2)
         plan.stage(2, dt, tarr, Q, work)
         hout.copy_(Q, non_blocking=True)
         torch.cuda.synchronize()

@@ -84,7 +84,10 @@ struct E2 {
     static constexpr int NL = N + 1;                          // levels per layer
     static constexpr int RING = 2 * N + 1;                    // level slots (two layers)
     static constexpr int PL = LY * LXT;                       // one field plane of a level
-    static constexpr int SS = (6 * PL + 15) / 16 * 16;        // slot stride (128-byte aligned)
+    // P' plane of a slot at a 128-byte aligned offset (it can arrive by its own TMA)
+    static constexpr int PPO = (5 * PL + 15) / 16 * 16;
+    static constexpr int SS = (PPO + PL + 15) / 16 * 16;      // slot stride (128-byte aligned)
+    __host__ __device__ static constexpr int foff(int f) { return f < 5 ? f * PL : PPO; }
 #ifdef HEVI_X_K
     static constexpr int K = HEVI_X_K;
 #else
@@ -108,6 +111,7 @@ struct E2 {
     }
     static constexpr int NTAB = 12;                           // level tables in smem
     static constexpr uint32_t LVL_BYTES = (uint32_t)(sizeof(double) * 5 * PL);   // one level TMA
+    static constexpr uint32_t PP_BYTES = (uint32_t)(sizeof(double) * PL);        // its P' plane
 };
 
 // smem level tables
@@ -280,7 +284,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
         if (want_xy) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const double* sx = bx_[k] + f * SF;
+                const double* sx = bx_[k] + T::foff(f);
                 double d = line_sum<N, 1>(D.x, sx);
                 if (MAIN && !(((HEVI_X_MERGE_MASK >> MODE) & 1) && f == 5)) {
                     // branch-free: the XF slot is in bounds for every main point
@@ -288,7 +292,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                     d += ax.face ? xf : 0.0;
                 } else if (ax.face) {
                     {
-                        const double* sxl = bxl_[k] + f * SF;
+                        const double* sxl = bxl_[k] + T::foff(f);
                         double e = 0.0;
 #pragma unroll
                         for (int m = 0; m <= N; ++m) e = fma(sDx[N * (N + 1) + m], sxl[m], e);
@@ -296,10 +300,10 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                     }
                 }
                 gxv[k] = cx * d;
-                const double* sy = by_[k] + f * SF;
+                const double* sy = by_[k] + T::foff(f);
                 double e = line_sum<NY, LXT>(D.y, sy);
                 if (ay.face) {
-                    const double* syl = byl_[k] + f * SF;
+                    const double* syl = byl_[k] + T::foff(f);
                     double h = 0.0;
 #pragma unroll
                     for (int m = 0; m <= NY; ++m) h = fma(sDy[NY * (NY + 1) + m], syl[m * LXT], h);
@@ -316,7 +320,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                 val[m] = LT[(base + m) * T::NTAB + T_G0] * bz_[m][0] + LT[(base + m) * T::NTAB + T_H0] * bz_[m][4 * SF];
         } else {
 #pragma unroll
-            for (int m = 0; m <= N; ++m) val[m] = bz_[m][f * SF];
+            for (int m = 0; m <= N; ++m) val[m] = bz_[m][T::foff(f)];
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -513,7 +517,8 @@ __device__ __forceinline__ void stage_level_manual(double* slot, const EArgs& a,
 template <int N, int NY, int TX, int TY, int MODE, int MINB>
 __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     k_explicit2(const EArgs a, const __grid_constant__ CUtensorMap tmap,
-                const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmF) {
+                const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmF,
+                const __grid_constant__ CUtensorMap tmP) {
     using T = E2<N, NY, TX, TY>;
     constexpr int PL = T::PL, LXT = T::LXT, RING = T::RING, SS = T::SS, BLK = T::BLK;
     constexpr bool NEED_R = (MODE != M_L);
@@ -571,13 +576,22 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     const int tx0 = txr - xsh;
     double* S = Sa + xsh;             // compute view: column lx at S[... + lx]
     const bool use_tma = a.use_tma != 0;
+    // stages 1 and 2: P' of the stage input was written by the column solve
+    // and arrives with each level (its own 1-field TMA) instead of being formed here
+    const bool pp_tma = use_tma && a.pp_in != nullptr && (MODE == M_S2 || MODE == M_S3);
+    const uint32_t lvl_bytes = T::LVL_BYTES + (pp_tma ? T::PP_BYTES : 0u);
+    auto load_level = [&](int L, uint64_t* bar) {
+        double* slot = Sa + (L % RING) * SS;
+        tma_load_4d(slot, &tmap, bar, tx0, ty0, L, 0);
+        if (pp_tma) tma_load_4d(slot + T::PPO, &tmP, bar, tx0, ty0, L, 0);
+    };
     // layers 0 and 1 in flight before the sweep starts (levels 0..2N, slots 0..2N)
     if (use_tma && tid == 0) {
-        mbar_expect_tx(&mbar[0], (N + 1) * T::LVL_BYTES);
-        for (int l = 0; l <= N; ++l) tma_load_4d(Sa + l * SS, &tmap, &mbar[0], tx0, ty0, l, 0);
+        mbar_expect_tx(&mbar[0], (N + 1) * lvl_bytes);
+        for (int l = 0; l <= N; ++l) load_level(l, &mbar[0]);
         if (g.nez > 1) {
-            mbar_expect_tx(&mbar[1], N * T::LVL_BYTES);
-            for (int l = N + 1; l <= 2 * N; ++l) tma_load_4d(Sa + l * SS, &tmap, &mbar[1], tx0, ty0, l, 0);
+            mbar_expect_tx(&mbar[1], N * lvl_bytes);
+            for (int l = N + 1; l <= 2 * N; ++l) load_level(l, &mbar[1]);
         }
     }
 
@@ -641,7 +655,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
             __syncthreads();
         }
         PH(0);
-        if (NEED_R) {
+        if (NEED_R && !pp_tma) {
             const int nconv = (N + 1 - lz0) * T::LY * T::LX;
             for (int idx = tid; idx < nconv; idx += BLK) {
                 const int lx = idx % T::LX;
@@ -650,7 +664,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                 const int gz = base + lz0 + t / T::LY;
                 double* sp = S + (gz % RING) * SS + ly * LXT + lx;
                 const double* lt = LT + gz * T::NTAB;
-                sp[5 * PL] = pprime(sp[0], sp[4 * PL], lt[T_RHO0], lt[T_TH0], lt[T_E0], lt[T_C0],
+                sp[T::PPO] = pprime(sp[0], sp[4 * PL], lt[T_RHO0], lt[T_TH0], lt[T_E0], lt[T_C0],
                                     lt[T_IRT0], lt[T_P0F], bc, a.ph);
             }
         }
@@ -664,7 +678,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                 t /= T::OYM;
                 const int ae = t % TX;
                 const int f = t / TX;
-                const double* sx = S + f * PL + ((base + oz) % RING) * SS + (oy + NY) * LXT + ae * N;
+                const double* sx = S + T::foff(f) + ((base + oz) % RING) * SS + (oy + NY) * LXT + ae * N;
                 double s = 0.0;
 #pragma unroll
                 for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sx[m], s);
@@ -687,7 +701,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
                 t /= T::OYM;
                 const int ae = t % TX;
                 const int f = t / TX;
-                const double* sx = S + f * PL + ((base + oz) % RING) * SS + (oy + NY) * LXT + ae * N;
+                const double* sx = S + T::foff(f) + ((base + oz) % RING) * SS + (oy + NY) * LXT + ae * N;
                 double s = 0.0;
 #pragma unroll
                 for (int m = 0; m <= N; ++m) s = fma(sDx[N * (N + 1) + m], sx[m], s);
@@ -737,11 +751,8 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
         if (use_tma && tid == 0 && ez + 2 < g.nez) {
             // generic-proxy accesses of the slots are ordered before the async-proxy refill
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&mbar[ez & 1], N * T::LVL_BYTES);
-            for (int l = 1; l <= N; ++l) {
-                const int L = base + 2 * N + l;
-                tma_load_4d(Sa + (L % RING) * SS, &tmap, &mbar[ez & 1], tx0, ty0, L, 0);
-            }
+            mbar_expect_tx(&mbar[ez & 1], N * lvl_bytes);
+            for (int l = 1; l <= N; ++l) load_level(base + 2 * N + l, &mbar[ez & 1]);
         }
     }
 #ifdef HEVI_PHASE_TIMING

@@ -112,6 +112,7 @@ struct EArgs {
     int use_tma;     // 1: TMA staging (default); 0: cooperative loads
     int rk_final;    // M_RK: last stage (non-finite output check, imexcore.py:124-125)
     int af_tma;      // explicit_v2 M_S2/M_S3: A/F layer boxes by TMA (set by launch_e2)
+    const double* pp_in;   // M_S2/M_S3 (set2nc): P' plane of the stage input from the column solve
     unsigned long long* dbg;   // HEVI_PHASE_TIMING builds: per-phase clock64 sums
 };
 
@@ -129,6 +130,8 @@ struct SArgs {
     const double* P;       // predictor fields 0,3,4
     double* out;           // writes fields 0,3,4
     const double* src_uv;  // optional: copy u,v (with no-flux zeroing) from here
+    double* pp_out;        // optional (set2nc): P' of the solved state, one lattice plane
+    double bc[16];         // EOS series coefficients (as EArgs::bc)
 };
 
 __device__ __forceinline__ long long loff(const Geo& g, int gx, int gy, int gz) {
@@ -1163,6 +1166,10 @@ struct hevi_plan {
     double bc[16];
     int eqset = 0;   // 0: set2nc, 1: set2c
     int force_pivoted = 0;   // HEVI_OPT_FORCE_PIVOTED (tests of the fallback path)
+    // the column solve of stage s wrote P' of its output into the P buffer's
+    // field 1 + s of this workspace (the next explicit stage reads it)
+    int pp_ok[2] = {0, 0};
+    const double* pp_work = nullptr;
     unsigned long long* d_dbg = nullptr;
     bool use_v2 = true;
     bool use_tma = true;
@@ -1277,13 +1284,13 @@ PFN_encodeTiled_t encode_fn() {
 }
 
 // 4D map (x, y, level, field) over a rank's lattice array, box = one layer tile
-int make_tmap(CUtensorMap* m, const Geo& g, const double* base, int bx, int by, int bz) {
+int make_tmap(CUtensorMap* m, const Geo& g, const double* base, int bx, int by, int bz, int nf = 5) {
     PFN_encodeTiled_t enc = encode_fn();
     if (!enc) return fail("cuTensorMapEncodeTiled unavailable");
     if (((uintptr_t)base & 15) || (g.px & 1)) return fail("lattice arrays must be 16-byte aligned with even pitch");
-    cuuint64_t dims[4] = {(cuuint64_t)g.lX, (cuuint64_t)g.lY, (cuuint64_t)g.Z, 5};
+    cuuint64_t dims[4] = {(cuuint64_t)g.lX, (cuuint64_t)g.lY, (cuuint64_t)g.Z, (cuuint64_t)nf};
     cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.lY * g.px * 8, (cuuint64_t)g.fs * 8};
-    cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz, 5};
+    cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz, (cuuint32_t)nf};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1325,8 +1332,15 @@ int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) 
             if (rc) return rc;
             a2.af_tma = 1;
         }
+        CUtensorMap tP = tm;
+        if ((MODE == M_S2 || MODE == M_S3) && a.pp_in) {
+            rc = make_tmap(&tP, g, a.pp_in, T::LXT, T::LY, 1, 1);   // one level of the P' plane
+            if (rc) return rc;
+        } else {
+            a2.pp_in = nullptr;
+        }
         dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
-        kern<<<grid, T::BLK, smem, st>>>(a2, tm, tA, tF);
+        kern<<<grid, T::BLK, smem, st>>>(a2, tm, tA, tF, tP);
         CK(cudaGetLastError());
         done = true;
         return HEVI_OK;
@@ -1535,11 +1549,14 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
     a.P = a1.P;
     a.out = a1.out;
     a.src_uv = a1.src_uv;
+    a.pp_out = a1.pp_out;
+    a.lv = pl->lv;
+    memcpy(a.bc, pl->bc, sizeof(a.bc));
     const int T = 128;
     if (f->pivoted) {   // columnsolve.factor_with_fallback: pivoted dense factor
         a.LU2 = f->LUP;
         const size_t smp = sizeof(double) * ((size_t)V_NT * M + (size_t)M * M + (N + 1) * (N + 1) +
-                                             (size_t)M * T) + sizeof(int) * M;
+                                             6 * (size_t)M + (size_t)M * T) + sizeof(int) * M;
         if (smp > 225 * 1024) return fail("column too tall for the pivoted column kernel");
         auto kern = pl->eqset == 1 ? k_solve_piv<N, true> : k_solve_piv<N, false>;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
@@ -1551,7 +1568,7 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
         return HEVI_OK;
     }
     const size_t smem = sizeof(double) * ((size_t)V_NT * M + (size_t)M * (4 * N + 1) + M +
-                                          (N + 1) * (N + 1) + (size_t)M * T);
+                                          (N + 1) * (N + 1) + 6 * (size_t)M + (size_t)M * T);
     if (smem > 225 * 1024) return fail("column too tall for the v2 column kernel");
     static size_t attr = 0;
     if (attr < smem) {
@@ -1582,7 +1599,7 @@ int run_s2(const hevi_plan* pl, const Factor* f, const SArgs& a, cudaStream_t st
     done = false;
     if (!pl->use_v2 || (f->nb > 2 * pl->N + 1 && !f->pivoted)) return HEVI_OK;
     const size_t need = sizeof(double) * ((size_t)V_NT * pl->g.Z +
-                                          (size_t)pl->g.Z * (4 * pl->N + 1 + 1 + 128));
+                                          (size_t)pl->g.Z * (4 * pl->N + 1 + 1 + 6 + 128));
     if (need > 220 * 1024) return HEVI_OK;
     int rc = HEVI_OK;
     switch (pl->N) {
@@ -1600,7 +1617,8 @@ int run_s2(const hevi_plan* pl, const Factor* f, const SArgs& a, cudaStream_t st
     return rc;
 }
 
-int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st) {
+int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st, bool* v2 = nullptr) {
+    if (v2) *v2 = false;
     {
         if (pl->eqset == 1) {
             const Factor* f = find_factor(pl, a.lam);
@@ -1614,6 +1632,7 @@ int run_s(const hevi_plan* pl, const SArgs& a, cudaStream_t st) {
         bool done = false;
         if (f) {
             int rc = run_s2(pl, f, a, st, done);
+            if (v2) *v2 = done && rc == HEVI_OK;
             if (rc || done) return rc;
             if (f->pivoted) return fail("pivoted column factor needs the v2 column kernel");
         }
@@ -1923,6 +1942,7 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
     int mode;
     if (stage == 0) {
         mode = M_S1;
+        pl->pp_ok[0] = pl->pp_ok[1] = 0;   // a new step: the solves will refill the P' planes
         a.q = Q;
         a.P = P;
         a.Quv = Q1;
@@ -1940,6 +1960,7 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
         a.Quv = A;
         a.A = A;
         a.F = F;
+        if (pl->pp_ok[0] && pl->pp_work == work) a.pp_in = P + pl->g.fs;
         a.a_p = a_[3 * 2 + 1];
         a.at_p = at[3 * 2 + 1];
         a.cb = dt * b[1];
@@ -1948,6 +1969,7 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
         a.q = A;
         a.F = F;
         a.out = Q;
+        if (pl->pp_ok[1] && pl->pp_work == work) a.pp_in = P + 2 * pl->g.fs;
         a.cb = dt * b[2];
     } else {
         return fail("stage must be 0, 1 or 2");
@@ -1962,12 +1984,20 @@ int hevi_stage_solve(hevi_plan* pl, int stage, double lam, double* work, void* s
         g_err = "lam not factored (call hevi_factor first)";
         return HEVI_ENOFACTOR;
     }
+    if (stage != 0 && stage != 1) return fail("stage must be 0 or 1");
     const long long fs5 = 5 * pl->g.fs;
     SArgs a = base_sargs(pl, f);
     a.P = work + 3 * fs5;
     a.out = stage == 0 ? work : work + fs5;
     a.src_uv = nullptr;
-    return run_s(pl, a, (cudaStream_t)stream);
+    // set2nc: P' of the solved stage state into field 1 + stage of the P buffer
+    a.pp_out = pl->eqset == 0 ? work + 3 * fs5 + (1 + stage) * pl->g.fs : nullptr;
+    memcpy(a.bc, pl->bc, sizeof(a.bc));
+    bool v2 = false;
+    const int rc = run_s(pl, a, (cudaStream_t)stream, &v2);
+    pl->pp_ok[stage] = (rc == HEVI_OK && v2 && a.pp_out) ? 1 : 0;
+    pl->pp_work = work;
+    return rc;
 }
 
 int hevi_ark2_step(hevi_plan* pl, double dt, const double* tab, double* Q, double* work,

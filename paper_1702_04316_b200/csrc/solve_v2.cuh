@@ -27,7 +27,45 @@ struct S2Args {
     const double* P;       // predictor fields 0,3,4
     double* out;           // writes fields 0,3,4
     const double* src_uv;  // optional: copy u,v (with no-flux zeroing)
+    double* pp_out;        // optional (set2nc): P' of the solved state (next explicit stage reads it)
+    Lev lv;
+    double bc[16];
 };
+
+// the rare |delta| > 1/8 branch of pprime, out of line (keeps the column
+// kernel's register budget)
+__device__ __noinline__ double pprime_pow(double rho, double theta, double P0f, double P0, double R,
+                                          double gamma) {
+    return P0 * pow(rho * R * theta / P0, gamma) - P0f;
+}
+
+// P' of a solved point: the explicit kernel's pprime (explicit_v2.cuh) on the
+// same inputs, written once here instead of per staged point downstream
+// PT: per-level [rho0 | theta0 | 1/(rho0 theta0) | Pb | Pb - P0f | P0f] in shared memory
+__device__ __forceinline__ double solved_pprime(const S2Args& a, const double* PT, int M, int k,
+                                                double r, double th) {
+    const double rho0 = PT[k], th0 = PT[M + k];
+    const double delta = (r * th0 + th * (rho0 + r)) * PT[2 * M + k];
+    if (fabs(delta) <= 0.125) {
+        double s = a.bc[14];
+#pragma unroll
+        for (int j = 13; j >= 0; --j) s = fma(s, delta, a.bc[j]);
+        return fma(PT[3 * M + k], s * delta, PT[4 * M + k]);
+    }
+    return pprime_pow(rho0 + r, th0 + th, PT[5 * M + k], a.ph.P0, a.ph.R, a.ph.gamma);
+}
+
+__device__ __forceinline__ void load_pp_tables(const S2Args& a, double* PT, int M, int tid, int T) {
+    const Lev& lv = a.lv;
+    for (int i = tid; i < M; i += T) {
+        PT[i] = lv.rho0[i];
+        PT[M + i] = lv.theta0[i];
+        PT[2 * M + i] = lv.irt0[i];
+        PT[3 * M + i] = lv.E0[i];
+        PT[4 * M + i] = lv.c0[i];
+        PT[5 * M + i] = lv.P0f[i];
+    }
+}
 
 enum { V_G0 = 0, V_H0, V_F0Z, V_RG, V_CZ, V_COEF, V_UA, V_DEN, V_DTH0, V_IRHO0, V_IG0R, V_IG0,
        V_F0C, V_TH0, V_IFT, V_ITH0, V_NT };
@@ -51,11 +89,13 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     double* LU = tb + V_NT * M;        // M * W
     double* rU = LU + M * W;           // M
     double* sD = rU + M;               // (N+1)^2
-    double* Y = sD + (N + 1) * (N + 1);  // M * T
+    double* PT = sD + (N + 1) * (N + 1);  // 6 * M: P' level tables
+    double* Y = PT + 6 * M;            // M * T
     for (int i = tid; i < V_NT * M; i += T) tb[i] = a.tab[i];
     for (int i = tid; i < M * W; i += T) LU[i] = a.LU2[i];
     for (int i = tid; i < M; i += T) rU[i] = a.rU[i];
     for (int i = tid; i < (N + 1) * (N + 1); i += T) sD[i] = a.Dz[i];
+    load_pp_tables(a, PT, M, tid, T);
     __syncthreads();
 
     const int NYo = g.slab ? 1 : N;
@@ -198,6 +238,7 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
         Oo[o] = rho;
         Oo[o + 3 * fs] = w;
         Oo[o + 4 * fs] = th;
+        if (!SC && a.pp_out) a.pp_out[loff(g, gx, gy, 0) + o] = solved_pprime(a, PT, M, k, rho, th);
         if (a.src_uv) {
             const bool bx = (gx == 0) || (gx == g.X - 1);
             const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);
@@ -283,12 +324,14 @@ __global__ void __launch_bounds__(128) k_solve_piv(const S2Args a, const int* __
     double* tb = smp;                   // V_NT * M
     double* LU = tb + V_NT * M;         // M * M
     double* sD = LU + M * M;            // (N+1)^2
-    double* Y = sD + (N + 1) * (N + 1); // M * T
+    double* PT = sD + (N + 1) * (N + 1); // 6 * M
+    double* Y = PT + 6 * M;             // M * T
     int* sp = reinterpret_cast<int*>(Y + (size_t)M * T);   // M
     for (int i = tid; i < V_NT * M; i += T) tb[i] = a.tab[i];
     for (int i = tid; i < M * M; i += T) LU[i] = a.LU2[i];
     for (int i = tid; i < (N + 1) * (N + 1); i += T) sD[i] = a.Dz[i];
     for (int i = tid; i < M; i += T) sp[i] = piv[i];
+    load_pp_tables(a, PT, M, tid, T);
     __syncthreads();
 
     const int NYo = g.slab ? 1 : N;
@@ -390,6 +433,7 @@ __global__ void __launch_bounds__(128) k_solve_piv(const S2Args a, const int* __
         Oo[o] = rho;
         Oo[o + 3 * fs] = w;
         Oo[o + 4 * fs] = th;
+        if (!SC && a.pp_out) a.pp_out[loff(g, gx, gy, 0) + o] = solved_pprime(a, PT, M, k, rho, th);
         if (a.src_uv) {
             const bool bx = (gx == 0) || (gx == g.X - 1);
             const bool by = g.slab || (gy == 0) || (gy == g.Y - 1);

@@ -207,24 +207,37 @@ class DistributedStepper:
         t = self.Q if t is None else t
         return _view(t, self.owned_region(), self.block.window)
 
+    def stage_inputs(self, s):
+        """Arrays whose halos stage s reads: the stage state, plus (set2nc) the
+        P' plane the preceding column solve wrote into field s of the P
+        buffer (hevi_stage_solve), so the explicit kernel need not form it."""
+        W = self.work
+        if s == 0:
+            return [self.Q]
+        state = W[0] if s == 1 else W[1]
+        if self.plan.set_name == "set2c":
+            return [state]
+        return [state, W[3][s:s + 1]]
+
     def step_stages(self):
         """Generator over the 8 ordered sub-steps (3 exchanges, 3 explicit
         stages, 2 solves) so a single-process driver can interleave ranks."""
         p, Q, W = self.plan, self.Q, self.work
-        yield ("exchange", Q)
+        yield ("exchange", self.stage_inputs(0))
         p.stage(0, self.dt, self.tab, Q, W)
         p.stage_solve(0, self.lam, W)
-        yield ("exchange", W[0])
+        yield ("exchange", self.stage_inputs(1))
         p.stage(1, self.dt, self.tab, Q, W)
         p.stage_solve(1, self.lam, W)
-        yield ("exchange", W[1])
+        yield ("exchange", self.stage_inputs(2))
         p.stage(2, self.dt, self.tab, Q, W)
         yield ("done", None)
 
     def step(self):
-        for kind, t in self.step_stages():
+        for kind, ts in self.step_stages():
             if kind == "exchange":
-                self.exchange(t)
+                for t in ts:
+                    self.exchange(t)
 
 
 class LocalExchange:
@@ -263,6 +276,8 @@ def run_local_partitioned(steppers, exchange: LocalExchange, nsteps=1):
             kind = items[0][0]
             if kind == "done":
                 break
-            tensors = [it[1] for it in items]
-            for r in range(len(steppers)):
-                exchange.fill(r, tensors)
+            lists = [it[1] for it in items]
+            for j in range(len(lists[0])):
+                tensors = [lst[j] for lst in lists]
+                for r in range(len(steppers)):
+                    exchange.fill(r, tensors)
