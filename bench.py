@@ -409,7 +409,9 @@ def run_gpu(args):
                "storage_dof_per_s": 5 * mesh.n_nodes / (ms_step * 1e-3),
                "roofline": roof, "step_roofline": step_roof, "kernels": kern,
                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
-               "gpu_launches": 5 * args.steps}
+               # fused HEVI step: P' plane of Q + 3 explicit stages + 2 column solves
+               # (set2c and RK35: 5 launches)
+               "gpu_launches": (6 if (not rk and args.set == "set2nc") else 5) * args.steps}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -576,9 +576,10 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
     const int tx0 = txr - xsh;
     double* S = Sa + xsh;             // compute view: column lx at S[... + lx]
     const bool use_tma = a.use_tma != 0;
-    // stages 1 and 2: P' of the stage input was written by the column solve
-    // and arrives with each level (its own 1-field TMA) instead of being formed here
-    const bool pp_tma = use_tma && a.pp_in != nullptr && (MODE == M_S2 || MODE == M_S3);
+    // P' of the stage input (stage 0: hevi_stage's k_pp_plane; stages 1, 2:
+    // the column solve) arrives with each level (its own 1-field TMA) instead
+    // of being formed here for every staged point
+    const bool pp_tma = use_tma && a.pp_in != nullptr && (MODE == M_S1 || MODE == M_S2 || MODE == M_S3);
     const uint32_t lvl_bytes = T::LVL_BYTES + (pp_tma ? T::PP_BYTES : 0u);
     auto load_level = [&](int L, uint64_t* bar) {
         double* slot = Sa + (L % RING) * SS;

@@ -1130,6 +1130,29 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 #include "solve_v2.cuh"
 #include "imex3d.cuh"
 
+// P' plane of a lattice state over the plan's whole window (stage 0 of the
+// fused step: formed once per point here instead of for every staged,
+// halo-overlapped point inside the explicit kernel)
+struct BC16 {
+    double v[16];
+};
+
+__global__ void k_pp_plane(const Geo g, Lev lv, Phys ph, const double* __restrict__ q,
+                           double* __restrict__ pp, const BC16 bcv) {
+    const double* bc = bcv.v;
+    const long long n = (long long)g.Z * g.lY * g.lX;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % g.lX);
+        const long long t = i / g.lX;
+        const int y = (int)(t % g.lY);
+        const int k = (int)(t / g.lY);
+        const long long o = ((long long)k * g.lY + y) * g.px + x;
+        pp[o] = pprime(q[o], q[o + 4 * g.fs], lv.rho0[k], lv.theta0[k], lv.E0[k], lv.c0[k], lv.irt0[k],
+                       lv.P0f[k], bc, ph);
+    }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1333,7 +1356,7 @@ int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) 
             a2.af_tma = 1;
         }
         CUtensorMap tP = tm;
-        if ((MODE == M_S2 || MODE == M_S3) && a.pp_in) {
+        if ((MODE == M_S1 || MODE == M_S2 || MODE == M_S3) && a.pp_in) {
             rc = make_tmap(&tP, g, a.pp_in, T::LXT, T::LY, 1, 1);   // one level of the P' plane
             if (rc) return rc;
         } else {
@@ -1943,6 +1966,16 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
     if (stage == 0) {
         mode = M_S1;
         pl->pp_ok[0] = pl->pp_ok[1] = 0;   // a new step: the solves will refill the P' planes
+        if (pl->eqset == 0 && pl->use_v2) {
+            // P'(Q) into Q1 field 0: not written by stage 0 (it writes Q1 u, v),
+            // overwritten by the stage-0 solve afterwards
+            BC16 bcv;
+            memcpy(bcv.v, pl->bc, sizeof(bcv.v));
+            const long long n = (long long)pl->g.Z * pl->g.lY * pl->g.lX;
+            k_pp_plane<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(pl->g, pl->lv, pl->ph, Q, Q1, bcv);
+            CK(cudaGetLastError());
+            a.pp_in = Q1;
+        }
         a.q = Q;
         a.P = P;
         a.Quv = Q1;
