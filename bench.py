@@ -50,17 +50,19 @@ CONFIGS = {
 }
 
 # algorithmic HBM bytes per unique point, per launch: each field
-# read / written once; 8 B per fp64 value.  The column solves also write P' of
-# their output (one plane), which explicit stages 1 and 2 read instead of
-# forming it from rho', theta' for every staged (halo-overlapped) point.
+# read / written once; 8 B per fp64 value.  P' of each stage input is one
+# plane (stage 0: k_pp_plane; stages 1, 2: written by the column solves) that
+# the explicit kernels read instead of forming it for every staged
+# (halo-overlapped) point.
 KERNEL_BYTES_PER_POINT = {
-    "explicit_stage0": 8 * (5 + 15),
+    # stage 0 = k_pp_plane (reads rho', theta', writes P'(Q)) + the explicit kernel
+    "explicit_stage0": 8 * (2 + 1) + 8 * (5 + 1 + 15),
     "solve_stage0": 8 * (3 + 3 + 1),
     "explicit_stage1": 8 * (15 + 1 + 10),
     "solve_stage1": 8 * (3 + 3 + 1),
     "explicit_stage2": 8 * (10 + 1 + 5),
 }
-STEP_BYTES_PER_POINT = sum(KERNEL_BYTES_PER_POINT.values())   # 608 B
+STEP_BYTES_PER_POINT = sum(KERNEL_BYTES_PER_POINT.values())   # 640 B
 SURVEY_BYTES_PER_POINT = 640                                   # SURVEY 8(d) 16 state passes
 
 
