@@ -1137,20 +1137,26 @@ struct BC16 {
     double v[16];
 };
 
-__global__ void k_pp_plane(const Geo g, Lev lv, Phys ph, const double* __restrict__ q,
-                           double* __restrict__ pp, const BC16 bcv) {
-    const double* bc = bcv.v;
-    const long long n = (long long)g.Z * g.lY * g.lX;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % g.lX);
-        const long long t = i / g.lX;
-        const int y = (int)(t % g.lY);
-        const int k = (int)(t / g.lY);
-        const long long o = ((long long)k * g.lY + y) * g.px + x;
-        pp[o] = pprime(q[o], q[o + 4 * g.fs], lv.rho0[k], lv.theta0[k], lv.E0[k], lv.c0[k], lv.irt0[k],
-                       lv.P0f[k], bc, ph);
+// grid (x blocks, rows y, levels z): the level constants once per thread
+__global__ void __launch_bounds__(256) k_pp_plane(const Geo g, Lev lv, Phys ph, const double* __restrict__ q,
+                                                  double* __restrict__ pp, const BC16 bcv) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= g.lX) return;
+    const int k = blockIdx.z;
+    const long long o = ((long long)k * g.lY + blockIdx.y) * g.px + x;
+    const double r = q[o], th = q[o + 4 * g.fs];
+    const double rho0 = __ldg(lv.rho0 + k), th0 = __ldg(lv.theta0 + k);
+    const double delta = (r * th0 + th * (rho0 + r)) * __ldg(lv.irt0 + k);
+    double v;
+    if (fabs(delta) <= 0.125) {   // pprime (explicit_v2.cuh), the series branch
+        double sum = bcv.v[14];
+#pragma unroll
+        for (int j = 13; j >= 0; --j) sum = fma(sum, delta, bcv.v[j]);
+        v = fma(__ldg(lv.E0 + k), sum * delta, __ldg(lv.c0 + k));
+    } else {
+        v = pprime_pow(rho0 + r, th0 + th, __ldg(lv.P0f + k), ph.P0, ph.R, ph.gamma);
     }
+    pp[o] = v;
 }
 
 }  // namespace
@@ -1971,8 +1977,8 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
             // overwritten by the stage-0 solve afterwards
             BC16 bcv;
             memcpy(bcv.v, pl->bc, sizeof(bcv.v));
-            const long long n = (long long)pl->g.Z * pl->g.lY * pl->g.lX;
-            k_pp_plane<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(pl->g, pl->lv, pl->ph, Q, Q1, bcv);
+            const dim3 grid((pl->g.lX + 255) / 256, pl->g.lY, pl->g.Z);
+            k_pp_plane<<<grid, 256, 0, (cudaStream_t)stream>>>(pl->g, pl->lv, pl->ph, Q, Q1, bcv);
             CK(cudaGetLastError());
             a.pp_in = Q1;
         }
