@@ -38,6 +38,9 @@
 // one barrier per layer.  Measured at config 5: stage 0 (M_S1) 1.581 -> 1.548
 // ms, stage 2 (M_S3) 1.443 -> 1.402 ms, stage 1 (M_S2, with its A/F boxes
 // staged by TMA) 1.584 -> 1.537 ms (before the A/F staging it was slower).
+#ifndef HEVI_X_XF6
+#define HEVI_X_XF6 1   // with the P' plane staged, its face partials join the merged face phase (-1%)
+#endif
 #ifndef HEVI_X_MERGE_MASK
 #define HEVI_X_MERGE_MASK 63
 #endif
@@ -204,7 +207,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
                                        const double* __restrict__ sDy, const PAx& ax, const PAx& ay,
                                        int oz0, int ox, int oy, int gx, int gy, int ez, double cx,
                                        double cy, int Z, const double* __restrict__ sAF = nullptr,
-                                       uint64_t* mbaf = nullptr) {
+                                       uint64_t* mbaf = nullptr, bool xf5 = false) {
     using T = E2<N, NY, TX, TY>;
     constexpr int PL = T::PL, LXT = T::LXT, RING = T::RING, SS = T::SS;
     constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
@@ -286,7 +289,7 @@ __device__ __forceinline__ void e2_pts(const EArgs& a, const double* __restrict_
             for (int k = 0; k < K; ++k) {
                 const double* sx = bx_[k] + T::foff(f);
                 double d = line_sum<N, 1>(D.x, sx);
-                if (MAIN && !(((HEVI_X_MERGE_MASK >> MODE) & 1) && f == 5)) {
+                if (MAIN && !(((HEVI_X_MERGE_MASK >> MODE) & 1) && f == 5 && !xf5)) {
                     // branch-free: the XF slot is in bounds for every main point
                     const double xf = xfp[f * (TX * T::OYM * N) + k];
                     d += ax.face ? xf : 0.0;
@@ -671,7 +674,8 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
         }
         if ((HEVI_X_MERGE_MASK >> MODE) & 1) {
             // face partials of the 5 state fields need only the TMA data
-            constexpr int NXF5 = 5 * TX * T::OYM * N;
+            // (with the P' plane staged by TMA its face partials are formed here too)
+            const int NXF5 = ((HEVI_X_XF6 && pp_tma) ? 6 : 5) * TX * T::OYM * N;
             for (int it = tid; it < NXF5; it += BLK) {
                 const int oz = it % N;
                 int t = it / N;
@@ -716,7 +720,7 @@ __global__ void __launch_bounds__(E2<N, NY, TX, TY>::BLK, MINB)
         if (main_ok) {
             e2_pts<N, NY, TX, TY, MODE, true, K>(a, S, CARr, CARw, XF, LT, Dm, sDx, sDy, max_, may_,
                                                  moz, mox, moy, mgx, mgy, ez, mcx, mcy, Z,
-                                                 af_tma ? sAF : nullptr, &mbar[2]);
+                                                 af_tma ? sAF : nullptr, &mbar[2], HEVI_X_XF6 && pp_tma);
         }
         // points outside the main box: domain-end x column / y row, top level
         const int ozn = N + ((ez == g.nez - 1) ? 1 : 0);
