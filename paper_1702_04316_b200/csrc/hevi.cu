@@ -1148,7 +1148,12 @@ __global__ void __launch_bounds__(256) k_pp_plane(const Geo g, Lev lv, Phys ph, 
     const double rho0 = __ldg(lv.rho0 + k), th0 = __ldg(lv.theta0 + k);
     const double delta = (r * th0 + th * (rho0 + r)) * __ldg(lv.irt0 + k);
     double v;
-    if (fabs(delta) <= 0.125) {   // pprime (explicit_v2.cuh), the series branch
+    if (HEVI_PP_SHORT && fabs(delta) <= 0x1p-10) {   // pprime (explicit_v2.cuh), short series
+        double sum = bcv.v[5];
+#pragma unroll
+        for (int j = 4; j >= 0; --j) sum = fma(sum, delta, bcv.v[j]);
+        v = fma(__ldg(lv.E0 + k), sum * delta, __ldg(lv.c0 + k));
+    } else if (fabs(delta) <= 0.125) {   // the 15-term series branch
         double sum = bcv.v[14];
 #pragma unroll
         for (int j = 13; j >= 0; --j) sum = fma(sum, delta, bcv.v[j]);

@@ -46,6 +46,13 @@ __device__ __forceinline__ double solved_pprime(const S2Args& a, const double* P
                                                 double r, double th) {
     const double rho0 = PT[k], th0 = PT[M + k];
     const double delta = (r * th0 + th * (rho0 + r)) * PT[2 * M + k];
+    if (HEVI_PP_SHORT && fabs(delta) <= 0x1p-10) {
+        // |delta| <= 2^-10: the terms beyond delta^6 are below 1e-20 relative
+        double s = a.bc[5];
+#pragma unroll
+        for (int j = 4; j >= 0; --j) s = fma(s, delta, a.bc[j]);
+        return fma(PT[3 * M + k], s * delta, PT[4 * M + k]);
+    }
     if (fabs(delta) <= 0.125) {
         double s = a.bc[14];
 #pragma unroll
