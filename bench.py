@@ -321,11 +321,13 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    halo0 = ds.exchange.launches if world > 1 else 0
     t_start.record(stream)
     for k in range(args.steps):
         one_step(evs[k])
     t_end.record(stream)
     torch.cuda.synchronize()
+    halo_launches = (ds.exchange.launches - halo0) if world > 1 else 0
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
@@ -413,7 +415,9 @@ def run_gpu(args):
                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
                # fused HEVI step: P' plane of Q + 3 explicit stages + 2 column solves
                # (set2c and RK35: 5 launches)
-               "gpu_launches": (6 if (not rk and args.set == "set2nc") else 5) * args.steps}
+               # plus, at N > 1, rank 0's halo pack/unpack kernels
+               "gpu_launches": (6 if (not rk and args.set == "set2nc") else 5) * args.steps
+                               + halo_launches}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -135,6 +135,7 @@ class HaloExchange:
         self.group = group
         self.plan = plan
         self._bufs = {}
+        self.launches = 0   # halo pack/unpack kernels launched so far
 
     def _buf(self, key, shape, like):
         import torch
@@ -157,6 +158,7 @@ class HaloExchange:
                 if native:
                     shp = lambda r: (t.shape[0], t.shape[1], r[3] - r[2], r[1] - r[0])  # noqa: E731
                     sbuf = pack(self.plan, t, sreg, self._buf(("s", ip, peer), shp(sreg), t))
+                    self.launches += 1
                     rbuf = self._buf(("r", ip, peer), shp(rreg), t)
                 else:
                     sbuf = _view(t, sreg, w).contiguous()
@@ -169,6 +171,7 @@ class HaloExchange:
             for rreg, rbuf in recvs:
                 if native:
                     unpack(self.plan, t, rreg, rbuf)
+                    self.launches += 1
                 else:
                     _view(t, rreg, w).copy_(rbuf)
 
