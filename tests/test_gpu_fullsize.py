@@ -1,0 +1,88 @@
+"""Size-independent properties of the fused HEVI step at BASELINE config 5
+(176x176x10 elements, N=4, 20.4 M unique points), where the oracle cannot
+run: the bubble is centred in a square domain, so the exact solution is
+mirror-symmetric in x and in y and symmetric under the x<->y transpose
+(u <-> v); a re-run of the same steps must give the same bits.  The
+tolerance is the north-star one (relative L2 <= 1e-10 per field)."""
+import os
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+TOL = 1e-10
+NSTEPS = 3
+
+
+@pytest.fixture(scope="module")
+def cfg5_run():
+    from bench import CONFIGS
+    from paper_1702_04316_b200 import specgrid, euler, imexcore, cases
+    from paper_1702_04316_b200.plan import tableau_array
+    cfg = CONFIGS["cfg5"]
+    mesh = specgrid.build_box_mesh_3d(cfg["nx"], cfg["ny"], cfg["nz"], cfg["Lx"], cfg["Ly"],
+                                      cfg["Lz"], cfg["N"])
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    q0 = cases.bubble_lattice(mesh, ref, 0.5, cfg["centre"], cfg["radii"])
+    dt = cases.dt_for_courant(mesh, ref, q0, cfg["courant"])
+    tab = imexcore.ark2_tableau()
+    plan = disc.plan_for(ref)
+    plan.factor(tab.diag * dt)
+    tarr = tableau_array(tab)
+
+    def run():
+        Q = plan.zeros()
+        Q[..., :mesh.X].copy_(q0)
+        work = plan.workspace()
+        for _ in range(NSTEPS):
+            plan.step(dt, tarr, Q, work)
+        plan.check_flags()
+        torch.cuda.synchronize()
+        return Q[..., :mesh.X].clone()
+
+    q = run()
+    return mesh, q0, q, run
+
+
+def rel(a, b):
+    return float(torch.linalg.vector_norm(a - b) / max(float(torch.linalg.vector_norm(b)), 1e-300))
+
+
+def test_cfg5_state_finite_and_evolved(cfg5_run):
+    mesh, q0, q, _ = cfg5_run
+    assert tuple(q.shape) == (5, mesh.Z, mesh.Y, mesh.X)
+    assert bool(q.isfinite().all())
+    assert mesh.n_unique == 20_378_025
+    # the bubble has started to move: velocities are no longer zero
+    for f in (1, 2, 3):
+        assert float(q[f].abs().max()) > 0.0
+    assert rel(q[4], q0[4]) > 0.0
+
+
+def test_cfg5_mirror_symmetry(cfg5_run):
+    _, _, q, _ = cfg5_run
+    # x -> Lx - x: rho', v, w, theta' even, u odd; y -> Ly - y: v odd
+    for axis, odd in ((3, 1), (2, 2)):
+        m = q.flip(axis)
+        for f in range(5):
+            want = -m[f] if f == odd else m[f]
+            assert rel(q[f], want) <= TOL, (axis, f, rel(q[f], want))
+
+
+def test_cfg5_transpose_symmetry(cfg5_run):
+    _, _, q, _ = cfg5_run
+    t = q.transpose(2, 3)
+    for f, g in ((0, 0), (1, 2), (2, 1), (3, 3), (4, 4)):
+        assert rel(q[f], t[g]) <= TOL, (f, g, rel(q[f], t[g]))
+
+
+def test_cfg5_rerun_is_bitwise_identical(cfg5_run):
+    _, _, q, run = cfg5_run
+    assert torch.equal(run(), q)
