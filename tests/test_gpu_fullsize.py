@@ -2,7 +2,9 @@
 (176x176x10 elements, N=4, 20.4 M unique points), where the oracle cannot
 run: the bubble is centred in a square domain, so the exact solution is
 mirror-symmetric in x and in y and symmetric under the x<->y transpose
-(u <-> v); a re-run of the same steps must give the same bits.  The
+(u <-> v); a re-run of the same steps must give the same bits, and the
+4x2 column partition of the 8-GPU scaling run (ranks emulated in lock-step
+on one device) must give the single-GPU bits.  The
 tolerance is the north-star one (relative L2 <= 1e-10 per field)."""
 import os
 import sys
@@ -48,7 +50,7 @@ def cfg5_run():
         return Q[..., :mesh.X].clone()
 
     q = run()
-    return mesh, q0, q, run
+    return mesh, q0, q, run, (ref, disc, dt)
 
 
 def rel(a, b):
@@ -56,7 +58,7 @@ def rel(a, b):
 
 
 def test_cfg5_state_finite_and_evolved(cfg5_run):
-    mesh, q0, q, _ = cfg5_run
+    mesh, q0, q, _, _ = cfg5_run
     assert tuple(q.shape) == (5, mesh.Z, mesh.Y, mesh.X)
     assert bool(q.isfinite().all())
     assert mesh.n_unique == 20_378_025
@@ -67,7 +69,7 @@ def test_cfg5_state_finite_and_evolved(cfg5_run):
 
 
 def test_cfg5_mirror_symmetry(cfg5_run):
-    _, _, q, _ = cfg5_run
+    _, _, q, _, _ = cfg5_run
     # x -> Lx - x: rho', v, w, theta' even, u odd; y -> Ly - y: v odd
     for axis, odd in ((3, 1), (2, 2)):
         m = q.flip(axis)
@@ -77,12 +79,29 @@ def test_cfg5_mirror_symmetry(cfg5_run):
 
 
 def test_cfg5_transpose_symmetry(cfg5_run):
-    _, _, q, _ = cfg5_run
+    _, _, q, _, _ = cfg5_run
     t = q.transpose(2, 3)
     for f, g in ((0, 0), (1, 2), (2, 1), (3, 3), (4, 4)):
         assert rel(q[f], t[g]) <= TOL, (f, g, rel(q[f], t[g]))
 
 
 def test_cfg5_rerun_is_bitwise_identical(cfg5_run):
-    _, _, q, run = cfg5_run
+    _, _, q, run, _ = cfg5_run
     assert torch.equal(run(), q)
+
+
+def test_cfg5_partition_4x2_is_bitwise_single_gpu(cfg5_run):
+    from paper_1702_04316_b200 import distributed as dd
+    mesh, q0, q, _, (ref, disc, dt) = cfg5_run
+    px, py = dd.grid_for(8)
+    ex = dd.LocalExchange(mesh, px, py)
+    steppers = [dd.DistributedStepper(mesh, ref, disc, dt, px, py, r, exchange=ex)
+                for r in range(8)]
+    for s in steppers:
+        s.load_global(q0)
+    dd.run_local_partitioned(steppers, ex, nsteps=NSTEPS)
+    torch.cuda.synchronize()
+    for s in steppers:
+        s.plan.check_flags()
+        x0, x1, y0, y1 = s.owned_region()
+        assert torch.equal(s.owned()[..., :x1 - x0], q[:, :, y0:y1, x0:x1]), s.block.rank

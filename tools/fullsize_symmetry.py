@@ -1,6 +1,6 @@
 import sys; sys.path.insert(0, "tests"); sys.path.insert(0, ".")
 import test_gpu_fullsize as t
-mesh, q0, q, run = t.cfg5_run.__wrapped__()
+mesh, q0, q, run, _ = t.cfg5_run.__wrapped__()
 for axis, odd in ((3, 1), (2, 2)):
     m = q.flip(axis)
     print("mirror", axis, ["%.1e" % t.rel(q[f], -m[f] if f == odd else m[f]) for f in range(5)])
