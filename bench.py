@@ -244,6 +244,7 @@ def run_gpu(args):
         Q = plan.zeros()
         Q[..., :mesh.X].copy_(q0)
         work = plan.workspace()
+        plan.pp_refresh(Q, work)
         exch = None
         px, py = 1, 1
     else:
@@ -262,6 +263,14 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     names = list(KERNEL_BYTES_PER_POINT)
 
+    chain = plan.chains_pp
+    # algorithmic bytes: with the chained P' plane stage 0 reads it from the
+    # previous stage 2 (which writes it) instead of a separate k_pp_plane pass
+    kb = dict(KERNEL_BYTES_PER_POINT)
+    if chain:
+        kb["explicit_stage0"] = 8 * (5 + 1 + 15)
+        kb["explicit_stage2"] = 8 * (10 + 1 + 5 + 1)
+    step_bytes = sum(kb.values())
     rk = args.integrator == "rk35"
     if rk and world > 1:
         raise SystemExit("--integrator rk35 runs on one GPU")
@@ -274,7 +283,8 @@ def run_gpu(args):
             exch(0)
         if ev is not None:
             ev[0].record(stream)
-        plan.stage(0, dt, tarr, Q, work)
+        # P'(Q) chained from the previous step's stage 2 (explicit_col path)
+        plan.stage(0, dt, tarr, Q, work, pp_valid=chain)
         if ev is not None:
             ev[1].record(stream)
         plan.stage_solve(0, lam, work)
@@ -358,16 +368,20 @@ def run_gpu(args):
         avg = ktimes[n] / args.steps
         if avg <= 0.0:
             continue
-        gbs = KERNEL_BYTES_PER_POINT[n] * pts_rank / (avg * 1e-3) / 1e9
-        kern[n] = {"ms": round(avg, 4), "alg_bytes_per_point": KERNEL_BYTES_PER_POINT[n],
+        gbs = kb[n] * pts_rank / (avg * 1e-3) / 1e9
+        kern[n] = {"ms": round(avg, 4), "alg_bytes_per_point": kb[n],
                    "alg_GBps": round(gbs, 1), "share": round(ktimes[n] / elapsed, 4)}
     if rk:   # whole RK35 step: 5 fused R + Shu-Osher launches (13 reads + 5 writes per point)
         kern = {"rk35_step": {"ms": round(ms_step, 4), "alg_bytes_per_point": 8 * 5 * 18,
                               "alg_GBps": round(8 * 5 * 18 * pts_rank / (ms_step * 1e-3) / 1e9, 1),
                               "share": 1.0}}
-        KERNEL_BYTES_PER_POINT["rk35_step"] = 8 * 5 * 18
+        kb["rk35_step"] = 8 * 5 * 18
         ktimes = {"rk35_step": elapsed}
         names = ["rk35_step"]
+    if rk or args.set != "set2nc":
+        launches_per_step = 5
+    else:
+        launches_per_step = 8 if chain else 6
     dom = max(names, key=lambda n: ktimes[n])
     traffic = None
     summ = ncu_traffic()
@@ -376,10 +390,10 @@ def run_gpu(args):
     achieved = kern[dom]["alg_GBps"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "alg_bytes_per_launch": KERNEL_BYTES_PER_POINT[dom] * pts_rank,
+            "alg_bytes_per_launch": kb[dom] * pts_rank,
             "peak_source": peak_src}
-    step_gbs = STEP_BYTES_PER_POINT * pts_rank / (ms_step * 1e-3) / 1e9
-    step_roof = {"alg_bytes_per_point": STEP_BYTES_PER_POINT, "achieved_GBps": round(step_gbs, 1),
+    step_gbs = step_bytes * pts_rank / (ms_step * 1e-3) / 1e9
+    step_roof = {"alg_bytes_per_point": step_bytes, "achieved_GBps": round(step_gbs, 1),
                  "frac": round(step_gbs / peak, 4),
                  "survey_640B_frac": round(SURVEY_BYTES_PER_POINT * pts_rank / (ms_step * 1e-3)
                                            / 1e9 / peak, 4)}
@@ -413,11 +427,10 @@ def run_gpu(args):
                "storage_dof_per_s": 5 * mesh.n_nodes / (ms_step * 1e-3),
                "roofline": roof, "step_roofline": step_roof, "kernels": kern,
                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
-               # fused HEVI step: P' plane of Q + 3 explicit stages + 2 column solves
-               # (set2c and RK35: 5 launches)
-               # plus, at N > 1, rank 0's halo pack/unpack kernels
-               "gpu_launches": (6 if (not rk and args.set == "set2nc") else 5) * args.steps
-                               + halo_launches}
+               # fused HEVI step: 3 explicit stages (explicit_col: main + domain-end
+               # kernel each) + 2 column solves [+ the P' plane of Q when not chained]
+               # (set2c and RK35: 5 launches); plus, at N > 1, rank 0's halo kernels
+               "gpu_launches": launches_per_step * args.steps + halo_launches}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

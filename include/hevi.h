@@ -105,6 +105,21 @@ int hevi_stage_solve(hevi_plan *plan, int stage, double lam, double *work, void 
 /* imexcore.ark_imex_step (imexcore.py:385-414), single rank: Q <- step(Q) */
 int hevi_ark2_step(hevi_plan *plan, double dt, const double *tab, double *Q, double *work,
                    void *stream);
+/* As hevi_ark2_step; with flags & HEVI_STEP_PP_VALID the caller asserts that
+ * work's Q1 field 0 holds P'(Q) (euler.py:454-457), as the previous step's
+ * stage 2 writes it when hevi_step_chains_pp(plan) is 1, so stage 0 does not
+ * form it again.  Steady stepping (cli.py:224-241 hot loop) sets the flag
+ * after hevi_pp_refresh once per externally supplied state. */
+#define HEVI_STEP_PP_VALID 1u
+int hevi_ark2_step_ex(hevi_plan *plan, double dt, const double *tab, double *Q, double *work,
+                      unsigned flags, void *stream);
+/* hevi_stage with the HEVI_STEP_PP_VALID contract of hevi_ark2_step_ex (stage 0) */
+int hevi_stage_ex(hevi_plan *plan, int stage, double dt, const double *tab,
+                  double *Q, double *work, unsigned flags, void *stream);
+/* P'(Q) into work's Q1 field 0 (the plane the chained step reads) */
+int hevi_pp_refresh(hevi_plan *plan, const double *Q, double *work, void *stream);
+/* 1 if hevi_ark2_step_ex writes P'(Q^{n+1}) for the next step on this plan */
+int hevi_step_chains_pp(const hevi_plan *plan);
 
 /* imexcore.rk35_step (imexcore.py:111-126): SSP RK(5,3) explicit step,
  * Q <- step(Q); work = 4 lattice arrays.  The explicit reference the HEVI

@@ -1,0 +1,546 @@
+// explicit_col.cuh -- column-sweep explicit kernel for 3D boxes, N = 4
+// (included by hevi.cu inside its anonymous namespace, after explicit_v2.cuh).
+//
+// R(q) (euler.nonlinear_rhs set2nc, euler.py:438-497), L_V(q)
+// (euler.vertical_restriction, euler.py:313-371) and the fused ARK2 stage
+// epilogues (imexcore.ark_imex_step, imexcore.py:385-414), with the DSS
+// folded into the derivatives exactly as k_explicit2 does.
+//
+// Structure (one CTA per 4x4-element horizontal tile, one thread per owned
+// lattice column, 256 threads, sweeping the levels bottom-up):
+//   * every level of the tile (+ N halo points low side, 1 high side) arrives
+//     by TMA into a ring of S level slots (6 planes: rho', u, v, w, theta',
+//     P'); a slot is refilled S levels ahead as soon as its level is done;
+//   * the z-lines never touch shared memory after the window load: at each
+//     element layer a thread loads its column's N+1 levels of the 6 fields
+//     into a register window, and every vertical derivative of the layer is
+//     a register contraction with the D row of the level (uniform loads from
+//     the parameter bank); the element-face carry from the layer below is a
+//     register too;
+//   * x-lines are element lines starting on 32-byte boundaries: two 16-byte
+//     and one 8-byte shared load per field; the row pitch (22 doubles) makes
+//     the warp's 2 rows x 4 elements conflict-free; y-lines are broadcast
+//     across the warp's two rows (one wavefront per load);
+//   * element-face partial sums (row N of the left / lower element) of the
+//     next level are formed once per face by all threads and double-buffered
+//     across the per-level barrier;
+//   * the domain-end planes x = X-1 and y = Y-1 (0.3% of the points) are
+//     evaluated by k_ecol_edge, one thread per point, lines from global.
+// Per-level constants (reference state, metric factor cz, the D rows of the
+// vertical derivative, the EOS reference point) sit in a __grid_constant__
+// parameter block: warp-uniform indices, no shared-memory bandwidth.
+#pragma once
+
+#define EC_ZMAX 96
+enum { C_RHO0 = 0, C_TH0, C_DRHO0, C_DTH0, C_CZ, C_IRHO0, C_G0, C_H0, C_PB, C_C0, C_IRT0, C_P0F, EC_NT };
+
+struct LvlTab {
+    double v[EC_NT][EC_ZMAX];
+    double dx[81], dy[81], dz[81];   // (N+1)^2 derivative matrices, row-major
+    double dzs[EC_ZMAX][9];          // cz[l] * Dz[row(l)][m]: the level's scaled vertical D row
+    double czf[EC_ZMAX];             // cz[l] on a bottom element face (carry from below), else 0
+};
+
+template <int N>
+struct EC {
+    static constexpr int TX = 4, TY = 4;                      // elements per tile
+    static constexpr int OX = TX * N, OY = TY * N;            // owned columns
+    static constexpr int BLK = OX * OY;                       // one thread per column
+    static constexpr int LX = OX + N + 1, LY = OY + N + 1;    // staged extent
+    static constexpr int LXT = (LX + 1) / 2 * 2;              // TMA box x (16-byte multiple)
+    static constexpr int PL = LXT * LY;                       // one field plane
+    static constexpr int PPO = (5 * PL + 15) / 16 * 16;       // P' plane (128-byte aligned)
+    static constexpr int SS = (PPO + PL + 15) / 16 * 16;      // slot stride
+    static constexpr int S = 8;                               // ring slots
+    static constexpr int NXF = 6 * OY * TX, NYF = 6 * TY * OX;   // face partials per level
+    static constexpr int DN = (N + 1) * (N + 1);
+    static constexpr size_t SMEM =
+        sizeof(double) * ((size_t)S * SS + 2 * (NXF + NYF) + 2 * DN + OX + OY) + sizeof(uint64_t) * S + 128;
+    static constexpr uint32_t LVL_BYTES = (uint32_t)(sizeof(double) * 5 * PL);
+    static constexpr uint32_t PP_BYTES = (uint32_t)(sizeof(double) * PL);
+    __host__ __device__ static constexpr int foff(int f) { return f < 5 ? f * PL : PPO; }
+};
+
+// R(q), L_V(q) at one point, accumulated field by field from its derivative
+// values (euler.py:458-473, 333-361); the no-flux projection
+// (euler.py:494-496) on the domain faces
+struct PtSt {
+    double r, u, v, w, th, rho, rinv;
+};
+struct PtAcc {
+    double R0, R1, R2, R3, R4, divu, dwz, dPLz;
+};
+
+__device__ __forceinline__ void ec_fold(int f, double gx, double gy, double gz, const PtSt& p, PtAcc& c) {
+    switch (f) {
+        case 0: c.R0 = (p.u * gx + p.v * gy) + p.w * gz; break;
+        case 1: c.R1 = (p.u * gx + p.v * gy) + p.w * gz; c.divu = gx; break;
+        case 2: c.R2 = (p.u * gx + p.v * gy) + p.w * gz; c.divu += gy; break;
+        case 3: c.R3 = (p.u * gx + p.v * gy) + p.w * gz; c.divu += gz; c.dwz = gz; break;
+        case 4: c.R4 = (p.u * gx + p.v * gy) + p.w * gz; break;
+        case 5:
+            c.R1 += gx * p.rinv;
+            c.R2 += gy * p.rinv;
+            c.R3 += gz * p.rinv;
+            c.R0 += p.rho * c.divu;
+            break;
+        default: c.dPLz = gz; break;
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void ec_finish(const PtSt& p, const PtAcc& c, double rho0, double drho0,
+                                          double dth0, double irho0, double gr, bool bx, bool by, bool bz,
+                                          double (&Rv)[5], double (&Lv)[5]) {
+    constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
+    constexpr bool NEED_R = (MODE != M_L);
+#pragma unroll
+    for (int f = 0; f < 5; ++f) Rv[f] = Lv[f] = 0.0;
+    if (NEED_R) {
+        Rv[0] = -(c.R0 + p.w * drho0);
+        Rv[1] = bx ? 0.0 : -c.R1;
+        Rv[2] = by ? 0.0 : -c.R2;
+        Rv[3] = bz ? 0.0 : -(c.R3 + (p.r * p.rinv) * gr);
+        Rv[4] = -(c.R4 + p.w * dth0);
+    }
+    if (NEED_L) {
+        Lv[0] = -(p.w * drho0 + rho0 * c.dwz);
+        Lv[3] = bz ? 0.0 : -(c.dPLz * irho0 + (p.r * irho0) * gr);
+        Lv[4] = -(p.w * dth0);
+    }
+}
+
+// input checks of nonlinear_rhs (euler.py:445-446, 183-184) at one point
+__device__ __forceinline__ void ec_check(const EArgs& a, const PtSt& p, double th0) {
+    const double s = ((p.r + p.u) + (p.v + p.w)) + p.th;
+    if (!isfinite(s)) {
+        if (!(isfinite(p.r) && isfinite(p.u) && isfinite(p.v) && isfinite(p.w) && isfinite(p.th)))
+            atomicOr(a.flags, HEVI_F_NONFINITE_IN(a.stage));
+    }
+    if (!(p.rho > 0.0) || !(th0 + p.th > 0.0)) atomicOr(a.flags, HEVI_F_EOS(a.stage));
+}
+
+// P' of a point from the per-level EOS constants (pprime of explicit_v2.cuh)
+__device__ __forceinline__ double ec_pprime(const EArgs& a, const LvlTab& lt, int gz, double r,
+                                            double th) {
+    return pprime(r, th, lt.v[C_RHO0][gz], lt.v[C_TH0][gz], lt.v[C_PB][gz], lt.v[C_C0][gz],
+                  lt.v[C_IRT0][gz], lt.v[C_P0F][gz], a.bc, a.ph);
+}
+
+// fused ARK2 stage epilogues (imexcore.py:398-411) and the plain R / L outputs
+template <int MODE>
+__device__ __forceinline__ void ec_epilogue(const EArgs& a, const LvlTab& lt, long long o, int gz,
+                                            const PtSt& p, const double (&Rv)[5], const double (&Lv)[5],
+                                            const double (&Ai)[5], const double (&Fi)[5], bool bx,
+                                            bool by) {
+    const long long fs = a.g.fs;
+    if (MODE == M_R) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) a.out[o + f * fs] = Rv[f];
+    } else if (MODE == M_L) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) a.out[o + f * fs] = Lv[f];
+    } else if (MODE == M_S1) {
+        const double dt = a.dt;
+        const double qv[5] = {p.r, p.u, p.v, p.w, p.th};
+        double pr[5];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            pr[f] = qv[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+            a.A[o + f * fs] = qv[f] + dt * (a.a_a * (Rv[f] - Lv[f]) + a.at_a * Lv[f]);
+            a.F[o + f * fs] = qv[f] + a.cb * Rv[f];
+        }
+        a.P[o] = pr[0];
+        a.P[o + 3 * fs] = pr[3];
+        a.P[o + 4 * fs] = pr[4];
+        a.Quv[o + fs] = bx ? 0.0 : pr[1];
+        a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+    } else if (MODE == M_S2) {
+        const double dt = a.dt;
+        double pr[5];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            pr[f] = Ai[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+            a.F[o + f * fs] = Fi[f] + a.cb * Rv[f];
+        }
+        a.P[o] = pr[0];
+        a.P[o + 3 * fs] = pr[3];
+        a.P[o + 4 * fs] = pr[4];
+        a.Quv[o + fs] = bx ? 0.0 : pr[1];
+        a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+    } else if (MODE == M_S3) {
+        double qn[5];
+        bool fin = true;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            qn[f] = Fi[f] + a.cb * Rv[f];
+            fin = fin && isfinite(qn[f]);
+            a.out[o + f * fs] = qn[f];
+        }
+        if (!fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
+        // P' of the new state for the next step's stage 0 (replaces k_pp_plane)
+        if (a.pp_out && fin) a.pp_out[o] = ec_pprime(a, lt, gz, qn[0], qn[4]);
+    }
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(EC<N>::BLK, 1)
+    k_ecol(const EArgs a, const __grid_constant__ LvlTab lt, const __grid_constant__ CUtensorMap tmq,
+           const __grid_constant__ CUtensorMap tmp) {
+    using T = EC<N>;
+    constexpr int PL = T::PL, LXT = T::LXT, SS = T::SS, S = T::S, BLK = T::BLK;
+    constexpr int OX = T::OX, OY = T::OY, TX = T::TX, TY = T::TY;
+    constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
+    constexpr bool NEED_R = (MODE != M_L);
+    static_assert(N == 4, "x-line vector loads assume N = 4");
+    extern __shared__ __align__(128) unsigned char smraw[];
+    double* ring = reinterpret_cast<double*>(
+        smraw + ((128u - ((unsigned)__cvta_generic_to_shared(smraw) & 127u)) & 127u));
+    double* XFb = ring + S * SS;          // [2][NXF]  XF[f][oy][j]
+    double* YFb = XFb + 2 * T::NXF;       // [2][NYF]  YF[f][j][ox]
+    double* sD = YFb + 2 * T::NYF;        // Dx | Dy
+    double* sC = sD + 2 * T::DN;          // cx of the tile's columns | cy of its rows
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sC + OX + OY);
+
+    const Geo& g = a.g;
+    const int Z = g.Z;
+    const int tid = threadIdx.x;
+    const int ox = tid % OX, oy = tid / OX;
+    const int ex0 = g.ex_b + blockIdx.x * TX, ey0 = g.ey_b + blockIdx.y * TY;
+    const int gx = ex0 * N + ox, gy = ey0 * N + oy;
+    const bool own = gx < g.ex_e * N && gy < g.ey_e * N;
+    const int tx0 = (ex0 - 1) * N - g.x0, ty0 = (ey0 - 1) * N - g.y0;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmq) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmp) : "memory");
+    }
+    for (int i = tid; i < T::DN; i += BLK) {
+        sD[i] = a.Dx[i];
+        sD[T::DN + i] = a.Dy[i];
+    }
+    // metric factors through shared memory: a register loaded from global
+    // before the sweep would share a scoreboard with the per-level loads
+    if (tid < OX) sC[tid] = (ex0 * N + tid < g.X) ? a.cx[ex0 * N + tid] : 0.0;
+    else if (tid < OX + OY) sC[tid] = (ey0 * N + tid - OX < g.Y) ? a.cy[ey0 * N + tid - OX] : 0.0;
+    __syncthreads();
+    auto issue = [&](int l) {
+        double* slot = ring + (l % S) * SS;
+        uint64_t* bar = &mbar[l % S];
+        mbar_expect_tx(bar, T::LVL_BYTES + T::PP_BYTES);
+        tma_load_4d(slot, &tmq, bar, tx0, ty0, l, 0);
+        tma_load_4d(slot + T::PPO, &tmp, bar, tx0, ty0, l, 0);
+    };
+    if (tid == 0) {
+        for (int l = 0; l < S && l < Z; ++l) issue(l);
+    }
+
+    // per-thread constants
+    const int rx = ox % N, ry = oy % N;
+    // the thread's D rows scaled by its metric factors (and the face-partial weights)
+    const double cxv = own ? sC[ox] : 0.0, cyv = own ? sC[OX + oy] : 0.0;
+    double Dxr[N + 1], Dyr[N + 1];
+#pragma unroll
+    for (int m = 0; m <= N; ++m) {
+        Dxr[m] = cxv * sD[rx * (N + 1) + m];
+        Dyr[m] = cyv * sD[T::DN + ry * (N + 1) + m];
+    }
+    const double fxs = (rx == 0) ? cxv : 0.0, fys = (ry == 0) ? cyv : 0.0;
+    const bool bx = (gx == 0), by = (gy == 0);   // x = X-1 / y = Y-1: k_ecol_edge
+    const int lx = ox + N, ly = oy + N;
+    const int xo = ly * LXT + (lx - rx);   // x-line start (32-byte aligned)
+    const int yo = (ly - ry) * LXT + lx;   // y-line start
+    const int po = ly * LXT + lx;          // own point
+    const int xfo = oy * TX + ox / N;
+    const int yfo = (oy / N) * OX + ox;
+    const long long colo = (long long)(gy - g.y0) * g.px + (gx - g.x0);
+    const long long zs = (long long)g.lY * g.px;
+    const long long fs = g.fs;
+    const double gr = a.ph.g;
+
+    // element-face partials (row N of the left / lower element) of level l
+    auto faces = [&](int l, int buf) {
+        if (!NEED_R) return;
+        const double* slot = ring + (l % S) * SS;
+        double* xf = XFb + buf * T::NXF;
+        double* yf = YFb + buf * T::NYF;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            int i = tid + r * BLK;
+            if (i < T::NXF) {
+                const int f = i / (OY * TX), rem = i % (OY * TX);
+                const int yy = rem / TX, j = rem % TX;
+                const double* s = slot + T::foff(f) + (yy + N) * LXT + j * N;
+                const double2 v01 = *reinterpret_cast<const double2*>(s);
+                const double2 v23 = *reinterpret_cast<const double2*>(s + 2);
+                double d = lt.dx[N * (N + 1) + 0] * v01.x;
+                d = fma(lt.dx[N * (N + 1) + 1], v01.y, d);
+                d = fma(lt.dx[N * (N + 1) + 2], v23.x, d);
+                d = fma(lt.dx[N * (N + 1) + 3], v23.y, d);
+                d = fma(lt.dx[N * (N + 1) + 4], s[4], d);
+                xf[i] = d;
+            } else if (i < T::NXF + T::NYF) {
+                i -= T::NXF;
+                const int f = i / (TY * OX), rem = i % (TY * OX);
+                const int j = rem / OX, xx = rem % OX;
+                const double* s = slot + T::foff(f) + (j * N) * LXT + xx + N;
+                double d = lt.dy[N * (N + 1)] * s[0];
+#pragma unroll
+                for (int m = 1; m <= N; ++m) d = fma(lt.dy[N * (N + 1) + m], s[m * LXT], d);
+                yf[i] = d;
+            }
+        }
+    };
+
+    double W[6][N + 1];    // the column's window: levels base .. base+N of the 6 planes
+    double PLw[N + 1];     // linearised pressure G0 rho' + H0 theta' on the window
+    double car[7];         // row-N partials of the layer below (bottom face)
+#pragma unroll
+    for (int f = 0; f < 7; ++f) car[f] = 0.0;
+#pragma unroll
+    for (int m = 0; m <= N; ++m) {
+        PLw[m] = 0.0;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) W[f][m] = 0.0;
+    }
+
+    mbar_wait(&mbar[0], 0);
+    faces(0, 0);
+    __syncthreads();
+
+    int k = 0;
+    for (int l = 0; l < Z; ++l) {
+        const bool top = (l == Z - 1);
+        const int krow = top ? N : k;
+        if (k == 0 && !top) {
+            if (l > 0) {
+                // carries of the finished layer (row N of its element)
+#pragma unroll
+                for (int f = 0; f < 6; ++f) {
+                    double c = lt.dz[N * (N + 1)] * W[f][0];
+#pragma unroll
+                    for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], W[f][m], c);
+                    car[f] = c;
+                }
+                if (NEED_L) {
+                    double c = lt.dz[N * (N + 1)] * PLw[0];
+#pragma unroll
+                    for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], PLw[m], c);
+                    car[6] = c;
+                }
+            }
+#pragma unroll
+            for (int m = 1; m <= N; ++m) mbar_wait(&mbar[(l + m) % S], ((l + m) / S) & 1);
+#pragma unroll
+            for (int m = 0; m <= N; ++m) {
+                const double* sp = ring + ((l + m) % S) * SS + po;
+#pragma unroll
+                for (int f = 0; f < 6; ++f) W[f][m] = sp[T::foff(f)];
+                if (NEED_L) PLw[m] = lt.v[C_G0][l + m] * W[0][m] + lt.v[C_H0][l + m] * W[4][m];
+            }
+        }
+        const long long o = colo + (long long)l * zs;
+        double Ai[5] = {0, 0, 0, 0, 0}, Fi[5] = {0, 0, 0, 0, 0};
+        if (own) {
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                if (MODE == M_S2) Ai[f] = a.A[o + f * fs];
+                if (MODE == M_S2 || MODE == M_S3) Fi[f] = a.F[o + f * fs];
+            }
+        }
+        const double* slot = ring + (l % S) * SS;
+        const double* xfb = XFb + (l & 1) * T::NXF;
+        const double* yfb = YFb + (l & 1) * T::NYF;
+        double dzr[N + 1];
+#pragma unroll
+        for (int m = 0; m <= N; ++m) dzr[m] = lt.dzs[l][m];
+        const double czf = lt.czf[l];
+        const double rho0 = lt.v[C_RHO0][l];
+
+        // the point's own state (level krow of the window, read from its slot)
+        PtSt p;
+        p.r = slot[po];
+        p.u = slot[PL + po];
+        p.v = slot[2 * PL + po];
+        p.w = slot[3 * PL + po];
+        p.th = slot[4 * PL + po];
+        p.rho = rho0 + p.r;
+        p.rinv = NEED_R ? 1.0 / p.rho : 0.0;
+        PtAcc c;
+        c.R0 = c.R1 = c.R2 = c.R3 = c.R4 = c.divu = c.dwz = c.dPLz = 0.0;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            if (!NEED_R && f != 3) continue;
+            double gxv = 0.0, gyv = 0.0;
+            if (NEED_R) {
+                const double* s = slot + T::foff(f);
+                const double2 v01 = *reinterpret_cast<const double2*>(s + xo);
+                const double2 v23 = *reinterpret_cast<const double2*>(s + xo + 2);
+                double dx = Dxr[0] * v01.x;
+                dx = fma(Dxr[1], v01.y, dx);
+                dx = fma(Dxr[2], v23.x, dx);
+                dx = fma(Dxr[3], v23.y, dx);
+                dx = fma(Dxr[4], s[xo + 4], dx);
+                gxv = fma(fxs, xfb[f * (OY * TX) + xfo], dx);
+                double dy = Dyr[0] * s[yo];
+#pragma unroll
+                for (int m = 1; m <= N; ++m) dy = fma(Dyr[m], s[yo + m * LXT], dy);
+                gyv = fma(fys, yfb[f * (TY * OX) + yfo], dy);
+            }
+            double dz = dzr[0] * W[f][0];
+#pragma unroll
+            for (int m = 1; m <= N; ++m) dz = fma(dzr[m], W[f][m], dz);
+            ec_fold(f, gxv, gyv, fma(czf, car[f], dz), p, c);
+        }
+        if (NEED_L) {
+            double dz = dzr[0] * PLw[0];
+#pragma unroll
+            for (int m = 1; m <= N; ++m) dz = fma(dzr[m], PLw[m], dz);
+            ec_fold(6, 0.0, 0.0, fma(czf, car[6], dz), p, c);
+        }
+        if (own) {
+            if (NEED_R) ec_check(a, p, lt.v[C_TH0][l]);
+            double Rv[5], Lv[5];
+            ec_finish<MODE>(p, c, rho0, lt.v[C_DRHO0][l], lt.v[C_DTH0][l], lt.v[C_IRHO0][l], gr, bx, by,
+                            (l == 0) || top, Rv, Lv);
+            ec_epilogue<MODE>(a, lt, o, l, p, Rv, Lv, Ai, Fi, bx, by);
+        }
+        if (l + 1 < Z) faces(l + 1, (l + 1) & 1);
+        __syncthreads();
+        if (tid == 0 && l + S < Z) {
+            // generic-proxy reads of the slot are ordered before its async-proxy refill
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(l + S);
+        }
+        if (!top) k = (k + 1 == N) ? 0 : k + 1;
+    }
+}
+
+// the domain-end planes x = X-1 / y = Y-1 inside the rank's ownership: one
+// thread per point, element lines read from global memory (L2)
+template <int N>
+__device__ __forceinline__ double ec_gline(const double* f, long long off, long long stride,
+                                           const double* Drow) {
+    double d = Drow[0] * f[off];
+#pragma unroll
+    for (int m = 1; m <= N; ++m) d = fma(Drow[m], f[off + m * stride], d);
+    return d;
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(128) k_ecol_edge(const EArgs a, const __grid_constant__ LvlTab lt,
+                                                   int nxc, int nyr, int xlo, int ylo) {
+    constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
+    constexpr bool NEED_R = (MODE != M_L);
+    const Geo& G = a.g;
+    // points: nxc column points (x = X-1, y = ylo ..), then nyr row points (y = Y-1, x = xlo ..), per level
+    const long long per = (long long)nxc + nyr;
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= per * G.Z) return;
+    const int gz = (int)(id / per);
+    const int cc = (int)(id % per);
+    int gx, gy;
+    if (cc < nxc) {
+        gx = G.X - 1;
+        gy = ylo + cc;
+    } else {
+        gx = xlo + (cc - nxc);
+        gy = G.Y - 1;
+    }
+    const long long fs = G.fs;
+    const long long zs = (long long)G.lY * G.px;
+    const int ix = gx - G.x0, iy = gy - G.y0;
+    const long long o = (long long)gz * zs + (long long)iy * G.px + ix;
+    auto axis = [](int gi, int ne, int& row, int& s0, bool& face) {
+        if (gi == ne * N) {
+            row = N;
+            s0 = gi - N;
+            face = false;
+        } else {
+            row = gi % N;
+            s0 = gi - row;
+            face = (row == 0) && (gi > 0);
+        }
+    };
+    int rxw, sx, ryw, sy, rzw, sz;
+    bool fx, fy, fz;
+    axis(gx, G.nex, rxw, sx, fx);
+    axis(gy, G.ney, ryw, sy, fy);
+    axis(gz, G.nez, rzw, sz, fz);
+    double Dxr[N + 1], Dyr[N + 1], Dzr[N + 1], DxN[N + 1], DyN[N + 1], DzN[N + 1];
+#pragma unroll
+    for (int m = 0; m <= N; ++m) {
+        Dxr[m] = lt.dx[rxw * (N + 1) + m];
+        DxN[m] = lt.dx[N * (N + 1) + m];
+        Dyr[m] = lt.dy[ryw * (N + 1) + m];
+        DyN[m] = lt.dy[N * (N + 1) + m];
+        Dzr[m] = lt.dz[rzw * (N + 1) + m];
+        DzN[m] = lt.dz[N * (N + 1) + m];
+    }
+    const double cxv = __ldg(a.cx + gx), cyv = __ldg(a.cy + gy), czv = lt.v[C_CZ][gz];
+    const long long xl = (long long)gz * zs + (long long)iy * G.px + (sx - G.x0);
+    const long long xll = xl - N;
+    const long long yl = (long long)gz * zs + (long long)(sy - G.y0) * G.px + ix;
+    const long long yll = yl - (long long)N * G.px;
+    const long long zl = (long long)sz * zs + (long long)iy * G.px + ix;
+    const long long zll = zl - (long long)N * zs;
+    const double* q = a.q;
+    const double rho0 = lt.v[C_RHO0][gz];
+    PtSt p;
+    p.r = q[o];
+    p.u = q[o + fs];
+    p.v = q[o + 2 * fs];
+    p.w = q[o + 3 * fs];
+    p.th = q[o + 4 * fs];
+    p.rho = rho0 + p.r;
+    p.rinv = NEED_R ? 1.0 / p.rho : 0.0;
+    PtAcc c;
+    c.R0 = c.R1 = c.R2 = c.R3 = c.R4 = c.divu = c.dwz = c.dPLz = 0.0;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+        if (!NEED_R && f != 3) continue;
+        const double* F = f < 5 ? q + f * fs : a.pp_in;
+        double gxv = 0.0, gyv = 0.0;
+        if (NEED_R) {
+            double dx = ec_gline<N>(F, xl, 1, Dxr);
+            if (fx) dx += ec_gline<N>(F, xll, 1, DxN);
+            gxv = cxv * dx;
+            double dy = ec_gline<N>(F, yl, G.px, Dyr);
+            if (fy) dy += ec_gline<N>(F, yll, G.px, DyN);
+            gyv = cyv * dy;
+        }
+        double dz = ec_gline<N>(F, zl, zs, Dzr);
+        if (fz) dz += ec_gline<N>(F, zll, zs, DzN);
+        ec_fold(f, gxv, gyv, czv * dz, p, c);
+    }
+    if (NEED_L) {
+        auto pl = [&](long long off, int lz) {
+            return lt.v[C_G0][lz] * q[off] + lt.v[C_H0][lz] * q[off + 4 * fs];
+        };
+        double dz = Dzr[0] * pl(zl, sz);
+#pragma unroll
+        for (int m = 1; m <= N; ++m) dz = fma(Dzr[m], pl(zl + m * zs, sz + m), dz);
+        if (fz) {
+            double e = DzN[0] * pl(zll, sz - N);
+#pragma unroll
+            for (int m = 1; m <= N; ++m) e = fma(DzN[m], pl(zll + m * zs, sz - N + m), e);
+            dz += e;
+        }
+        ec_fold(6, 0.0, 0.0, czv * dz, p, c);
+    }
+    if (NEED_R) ec_check(a, p, lt.v[C_TH0][gz]);
+    const bool bx = (gx == 0) || (gx == G.X - 1);
+    const bool by = (gy == 0) || (gy == G.Y - 1);
+    const bool bz = (gz == 0) || (gz == G.Z - 1);
+    double Rv[5], Lv[5];
+    ec_finish<MODE>(p, c, rho0, lt.v[C_DRHO0][gz], lt.v[C_DTH0][gz], lt.v[C_IRHO0][gz], a.ph.g, bx, by, bz,
+                    Rv, Lv);
+    double Ai[5] = {0, 0, 0, 0, 0}, Fi[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+        if (MODE == M_S2) Ai[f] = a.A[o + f * fs];
+        if (MODE == M_S2 || MODE == M_S3) Fi[f] = a.F[o + f * fs];
+    }
+    ec_epilogue<MODE>(a, lt, o, gz, p, Rv, Lv, Ai, Fi, bx, by);
+}

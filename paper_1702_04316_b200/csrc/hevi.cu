@@ -113,6 +113,7 @@ struct EArgs {
     int rk_final;    // M_RK: last stage (non-finite output check, imexcore.py:124-125)
     int af_tma;      // explicit_v2 M_S2/M_S3: A/F layer boxes by TMA (set by launch_e2)
     const double* pp_in;   // M_S2/M_S3 (set2nc): P' plane of the stage input from the column solve
+    double* pp_out;        // explicit_col M_S3: P' plane of the new state (next step's stage 0)
     unsigned long long* dbg;   // HEVI_PHASE_TIMING builds: per-phase clock64 sums
 };
 
@@ -1126,6 +1127,7 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 }
 
 #include "explicit_v2.cuh"
+#include "explicit_col.cuh"
 #include "explicit_c.cuh"
 #include "solve_v2.cuh"
 #include "imex3d.cuh"
@@ -1207,6 +1209,9 @@ struct hevi_plan {
     unsigned long long* d_dbg = nullptr;
     bool use_v2 = true;
     bool use_tma = true;
+    bool use_col = true;     // explicit_col kernels (3D, N = 4, set2nc)
+    bool lt_ok = false;      // lt filled (Z <= EC_ZMAX)
+    LvlTab lt;               // per-level constants of the explicit_col kernels
 };
 
 namespace {
@@ -1487,6 +1492,63 @@ int dispatch_c(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     return fail("set2c: unsupported polynomial order for the device path");
 }
 
+// ---- explicit_col dispatch (3D box, N = 4, set2nc, stage kernels) --------
+// cudaFuncSetAttribute once per (kernel, device)
+template <typename K>
+int set_smem_attr(K kern, size_t smem, size_t (&done)[16]) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 16) return fail("device index out of range");
+    if (done[dev] < smem) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        done[dev] = smem;
+    }
+    return HEVI_OK;
+}
+
+bool col_applies(const hevi_plan* pl, int mode, const EArgs& a) {
+    const Geo& g = pl->g;
+    return pl->use_col && pl->use_tma && pl->lt_ok && pl->eqset == 0 && pl->N == 4 && pl->Ny == 4 &&
+           !g.slab && (g.x0 % 2) == 0 && (g.px % 2) == 0 && a.pp_in != nullptr &&
+           (mode == M_S1 || mode == M_S2 || mode == M_S3 || mode == M_R);
+}
+
+template <int N, int MODE>
+int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
+    using T = EC<N>;
+    const Geo& g = pl->g;
+    static size_t attr[16] = {0};
+    auto kern = k_ecol<N, MODE>;
+    int rc = set_smem_attr(kern, T::SMEM, attr);
+    if (rc) return rc;
+    CUtensorMap tq, tp;
+    if ((rc = make_tmap(&tq, g, a.q, T::LXT, T::LY, 1))) return rc;
+    if ((rc = make_tmap(&tp, g, a.pp_in, T::LXT, T::LY, 1, 1))) return rc;
+    const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
+    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp);
+    CK(cudaGetLastError());
+    // domain-end planes owned by this rank
+    const int nxc = (g.ex_e == g.nex) ? (g.ey_e - g.ey_b) * N + (g.ey_e == g.ney ? 1 : 0) : 0;
+    const int nyr = (g.ey_e == g.ney) ? (g.ex_e - g.ex_b) * N : 0;
+    const long long npt = (long long)(nxc + nyr) * g.Z;
+    if (npt > 0) {
+        k_ecol_edge<N, MODE><<<(unsigned)((npt + 127) / 128), 128, 0, st>>>(a, pl->lt, nxc, nyr, g.ex_b * N,
+                                                                          g.ey_b * N);
+        CK(cudaGetLastError());
+    }
+    return HEVI_OK;
+}
+
+int run_col(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
+    switch (mode) {
+        case M_R: return launch_col<4, M_R>(pl, a, st);
+        case M_S1: return launch_col<4, M_S1>(pl, a, st);
+        case M_S2: return launch_col<4, M_S2>(pl, a, st);
+        case M_S3: return launch_col<4, M_S3>(pl, a, st);
+    }
+    return fail("bad mode");
+}
+
 int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
     if (pl->eqset == 1) {
         switch (mode) {
@@ -1499,6 +1561,7 @@ int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
         }
         return fail("bad mode");
     }
+    if (col_applies(pl, mode, a)) return run_col(pl, mode, a, st);
     if (pl->use_v2 && (pl->g.px % 2) == 0) {
         bool done = false;
         int rc = run_e2(pl, mode, a, st, done);
@@ -1825,6 +1888,35 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     }
     pl->use_v2 = getenv("HEVI_KERNELS") == nullptr || strcmp(getenv("HEVI_KERNELS"), "v1") != 0;
     pl->use_tma = getenv("HEVI_NO_TMA") == nullptr;
+    pl->use_col = pl->use_v2 && (getenv("HEVI_KERNELS") == nullptr || strcmp(getenv("HEVI_KERNELS"), "v2") != 0);
+    if (Z <= EC_ZMAX && nd <= 81 && ndy <= 81) {
+        LvlTab& t = pl->lt;
+        memset(&t, 0, sizeof(t));
+        for (int k = 0; k < Z; ++k) {
+            t.v[C_RHO0][k] = rd->rho0[k];
+            t.v[C_TH0][k] = rd->theta0[k];
+            t.v[C_DRHO0][k] = rd->drho0[k];
+            t.v[C_DTH0][k] = rd->dtheta0[k];
+            t.v[C_CZ][k] = rd->cz[k];
+            t.v[C_IRHO0][k] = 1.0 / rd->rho0[k];
+            t.v[C_G0][k] = rd->G0[k];
+            t.v[C_H0][k] = rd->H0[k];
+            t.v[C_PB][k] = rd->Pb[k];
+            t.v[C_C0][k] = rd->Pb[k] - rd->P0f[k];
+            t.v[C_IRT0][k] = 1.0 / (rd->rho0[k] * rd->theta0[k]);
+            t.v[C_P0F][k] = rd->P0f[k];
+        }
+        memcpy(t.dx, rd->Dx, sizeof(double) * nd);
+        memcpy(t.dy, rd->Dy, sizeof(double) * ndy);
+        memcpy(t.dz, rd->Dz, sizeof(double) * nd);
+        const int N = gd->N;
+        for (int k = 0; k < Z; ++k) {
+            const int row = (k == Z - 1) ? N : k % N;
+            for (int m = 0; m <= N; ++m) t.dzs[k][m] = rd->cz[k] * rd->Dz[row * (N + 1) + m];
+            t.czf[k] = (row == 0 && k > 0) ? rd->cz[k] : 0.0;
+        }
+        pl->lt_ok = true;
+    }
     *out = pl;
     return HEVI_OK;
 }
@@ -1959,8 +2051,27 @@ int hevi_solve(hevi_plan* pl, double lam, const double* qe, double* q, void* str
     return run_s(pl, a, (cudaStream_t)stream);
 }
 
-int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q, double* work,
-               void* stream) {
+// the fused step chains P' of the stage-0 input through stage 2 of the
+// previous step (explicit_col M_S3 writes P'(Q^{n+1}) into work's Q1 field 0)
+static bool pp_chainable(const hevi_plan* pl) {
+    const Geo& g = pl->g;
+    return pl->use_col && pl->use_v2 && pl->use_tma && pl->lt_ok && pl->eqset == 0 && pl->N == 4 &&
+           pl->Ny == 4 && !g.slab && (g.x0 % 2) == 0 && (g.px % 2) == 0;
+}
+
+int hevi_pp_refresh(hevi_plan* pl, const double* Q, double* work, void* stream) {
+    if (!pl || !Q || !work) return fail("null argument");
+    if (pl->eqset != 0) return HEVI_OK;
+    BC16 bcv;
+    memcpy(bcv.v, pl->bc, sizeof(bcv.v));
+    const dim3 grid((pl->g.lX + 255) / 256, pl->g.lY, pl->g.Z);
+    k_pp_plane<<<grid, 256, 0, (cudaStream_t)stream>>>(pl->g, pl->lv, pl->ph, Q, work, bcv);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+static int stage_impl(hevi_plan* pl, int stage, double dt, const double* tab, double* Q, double* work,
+                      bool pp_chain, void* stream) {
     if (!pl || !tab || !Q || !work) return fail("null argument");
     const long long fs5 = 5 * pl->g.fs;
     double* Q1 = work;
@@ -1979,12 +2090,12 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
         pl->pp_ok[0] = pl->pp_ok[1] = 0;   // a new step: the solves will refill the P' planes
         if (pl->eqset == 0 && pl->use_v2) {
             // P'(Q) into Q1 field 0: not written by stage 0 (it writes Q1 u, v),
-            // overwritten by the stage-0 solve afterwards
-            BC16 bcv;
-            memcpy(bcv.v, pl->bc, sizeof(bcv.v));
-            const dim3 grid((pl->g.lX + 255) / 256, pl->g.lY, pl->g.Z);
-            k_pp_plane<<<grid, 256, 0, (cudaStream_t)stream>>>(pl->g, pl->lv, pl->ph, Q, Q1, bcv);
-            CK(cudaGetLastError());
+            // overwritten by the stage-0 solve afterwards; with pp_chain the
+            // previous step's stage 2 already wrote it there
+            if (!pp_chain) {
+                int rc = hevi_pp_refresh(pl, Q, Q1, stream);
+                if (rc) return rc;
+            }
             a.pp_in = Q1;
         }
         a.q = Q;
@@ -2014,11 +2125,24 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
         a.F = F;
         a.out = Q;
         if (pl->pp_ok[1] && pl->pp_work == work) a.pp_in = P + 2 * pl->g.fs;
+        // Q1 is dead after stage 1: its field 0 takes P'(Q^{n+1}) (explicit_col only)
+        a.pp_out = Q1;
         a.cb = dt * b[2];
     } else {
         return fail("stage must be 0, 1 or 2");
     }
     return run_e(pl, mode, a, (cudaStream_t)stream);
+}
+
+int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q, double* work,
+               void* stream) {
+    return stage_impl(pl, stage, dt, tab, Q, work, false, stream);
+}
+
+int hevi_stage_ex(hevi_plan* pl, int stage, double dt, const double* tab, double* Q, double* work,
+                  unsigned flags, void* stream) {
+    const bool chain = stage == 0 && (flags & HEVI_STEP_PP_VALID) && pl && pp_chainable(pl);
+    return stage_impl(pl, stage, dt, tab, Q, work, chain, stream);
 }
 
 int hevi_stage_solve(hevi_plan* pl, int stage, double lam, double* work, void* stream) {
@@ -2044,18 +2168,26 @@ int hevi_stage_solve(hevi_plan* pl, int stage, double lam, double* work, void* s
     return rc;
 }
 
-int hevi_ark2_step(hevi_plan* pl, double dt, const double* tab, double* Q, double* work,
-                   void* stream) {
+int hevi_ark2_step_ex(hevi_plan* pl, double dt, const double* tab, double* Q, double* work,
+                      unsigned flags, void* stream) {
     if (!pl || !tab) return fail("null argument");
     const double lam = tab[9 + 3 * 1 + 1] * dt;  // problem.lam = tableau.diag * dt
     int rc = hevi_factor(pl, lam, nullptr, stream);
     if (rc) return rc;
-    if ((rc = hevi_stage(pl, 0, dt, tab, Q, work, stream))) return rc;
+    const bool chain = (flags & HEVI_STEP_PP_VALID) && pp_chainable(pl);
+    if ((rc = stage_impl(pl, 0, dt, tab, Q, work, chain, stream))) return rc;
     if ((rc = hevi_stage_solve(pl, 0, lam, work, stream))) return rc;
-    if ((rc = hevi_stage(pl, 1, dt, tab, Q, work, stream))) return rc;
+    if ((rc = stage_impl(pl, 1, dt, tab, Q, work, false, stream))) return rc;
     if ((rc = hevi_stage_solve(pl, 1, lam, work, stream))) return rc;
-    return hevi_stage(pl, 2, dt, tab, Q, work, stream);
+    return stage_impl(pl, 2, dt, tab, Q, work, false, stream);
 }
+
+int hevi_ark2_step(hevi_plan* pl, double dt, const double* tab, double* Q, double* work,
+                   void* stream) {
+    return hevi_ark2_step_ex(pl, dt, tab, Q, work, 0u, stream);
+}
+
+int hevi_step_chains_pp(const hevi_plan* pl) { return pl && pp_chainable(pl) ? 1 : 0; }
 
 int hevi_rk35_step(hevi_plan* pl, double dt, double* Q, double* work, void* stream) {
     if (!pl || !Q || !work) return fail("null argument");

@@ -192,12 +192,16 @@ class DistributedStepper:
         self.plan.factor(self.lam)
         self.Q = self.plan.zeros()
         self.work = self.plan.workspace()
+        # P'(Q) chained from stage 2 into the next step's stage 0; its halo is
+        # then exchanged with the state (stage_inputs(0))
+        self.chain = self.plan.chains_pp
 
     def load_global(self, q_lattice):
         """Copy this rank's window out of a global (5, Z, Y, X) lattice tensor."""
         w = self.block.window
         self.Q[:, :, :, :w["lX"]].copy_(
             q_lattice[:, :, w["y0"]:w["y0"] + w["lY"], w["x0"]:w["x0"] + w["lX"]])
+        self.plan.pp_refresh(self.Q, self.work)   # whole window, halos included
 
     def owned_region(self):
         m = self.plan.mesh
@@ -216,7 +220,7 @@ class DistributedStepper:
         buffer (hevi_stage_solve), so the explicit kernel need not form it."""
         W = self.work
         if s == 0:
-            return [self.Q]
+            return [self.Q, W[0][0:1]] if self.chain else [self.Q]
         state = W[0] if s == 1 else W[1]
         if self.plan.set_name == "set2c":
             return [state]
@@ -227,7 +231,7 @@ class DistributedStepper:
         stages, 2 solves) so a single-process driver can interleave ranks."""
         p, Q, W = self.plan, self.Q, self.work
         yield ("exchange", self.stage_inputs(0))
-        p.stage(0, self.dt, self.tab, Q, W)
+        p.stage(0, self.dt, self.tab, Q, W, pp_valid=self.chain)
         p.stage_solve(0, self.lam, W)
         yield ("exchange", self.stage_inputs(1))
         p.stage(1, self.dt, self.tab, Q, W)

@@ -156,16 +156,28 @@ class HeviPlan:
         nv.check(self.lib.hevi_solve(self.h, float(lam), nv.ptr(qe), nv.ptr(out), nv.stream_ptr()))
         return out
 
-    def step(self, dt, tab: np.ndarray, Q, work):
-        nv.check(self.lib.hevi_ark2_step(self.h, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
-                                         nv.stream_ptr()))
+    @property
+    def chains_pp(self) -> bool:
+        """Whether a fused step writes P'(Q^{n+1}) for the next step's stage 0
+        (the explicit_col path), so steady stepping may pass pp_valid."""
+        return bool(self.lib.hevi_step_chains_pp(self.h))
+
+    def pp_refresh(self, Q, work):
+        """P'(Q) into work's Q1 field 0 (the plane a chained stage 0 reads)."""
+        nv.check(self.lib.hevi_pp_refresh(self.h, nv.ptr(Q), nv.ptr(work), nv.stream_ptr()))
+
+    def step(self, dt, tab: np.ndarray, Q, work, pp_valid=False):
+        """One fused ARK2 step; ``pp_valid``: work's Q1 field 0 already holds
+        P'(Q) (written by the previous chained step or pp_refresh)."""
+        nv.check(self.lib.hevi_ark2_step_ex(self.h, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
+                                            nv.STEP_PP_VALID if pp_valid else 0, nv.stream_ptr()))
 
     def rk35(self, dt, Q, work):
         nv.check(self.lib.hevi_rk35_step(self.h, float(dt), nv.ptr(Q), nv.ptr(work), nv.stream_ptr()))
 
-    def stage(self, s, dt, tab: np.ndarray, Q, work):
-        nv.check(self.lib.hevi_stage(self.h, s, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
-                                     nv.stream_ptr()))
+    def stage(self, s, dt, tab: np.ndarray, Q, work, pp_valid=False):
+        nv.check(self.lib.hevi_stage_ex(self.h, s, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
+                                        nv.STEP_PP_VALID if pp_valid else 0, nv.stream_ptr()))
 
     def stage_solve(self, s, lam, work):
         nv.check(self.lib.hevi_stage_solve(self.h, s, float(lam), nv.ptr(work), nv.stream_ptr()))

@@ -20,6 +20,10 @@ class HeviStepper:
         self.check_every = check_every
         self.steps = 0
         self._graph = None
+        # P'(Q) chained from each step's stage 2 into the next stage 0
+        # (hevi_ark2_step_ex); refreshed whenever the state is replaced
+        self._chain = self.plan.chains_pp
+        self.plan.pp_refresh(self.Q, self.work)
 
     # state in / out ---------------------------------------------------------
     def set_state(self, q, lattice=False):
@@ -29,6 +33,7 @@ class HeviStepper:
             from .plan import to_device
             E, _ = to_device(q)
             self.plan.e2l(E, out=self.Q)
+        self.plan.pp_refresh(self.Q, self.work)
 
     def state(self, lattice=False):
         if lattice:
@@ -37,12 +42,16 @@ class HeviStepper:
 
     # stepping ---------------------------------------------------------------
     def _launch(self):
-        self.plan.step(self.dt, self.tab, self.Q, self.work)
+        self.plan.step(self.dt, self.tab, self.Q, self.work, pp_valid=self._chain)
 
     def capture(self):
-        """Record one step as a CUDA graph (5 kernel launches)."""
+        """Record one step as a CUDA graph.  The warm-up step that sets the
+        kernels' shared-memory attributes outside the capture is a real step:
+        it is counted and its flags are checked."""
         import torch
-        self._launch()  # warm: kernels' smem attributes are set outside capture
+        self._launch()
+        self.steps += 1
+        self.plan.check_flags()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
