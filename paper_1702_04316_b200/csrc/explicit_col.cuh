@@ -41,7 +41,7 @@ struct LvlTab {
     double czf[EC_ZMAX];             // cz[l] on a bottom element face (carry from below), else 0
 };
 
-template <int N>
+template <int N, int MODE>
 struct EC {
     static constexpr int TX = 4, TY = 4;                      // elements per tile
     static constexpr int OX = TX * N, OY = TY * N;            // owned columns
@@ -51,13 +51,19 @@ struct EC {
     static constexpr int PL = LXT * LY;                       // one field plane
     static constexpr int PPO = (5 * PL + 15) / 16 * 16;       // P' plane (128-byte aligned)
     static constexpr int SS = (PPO + PL + 15) / 16 * 16;      // slot stride
-    static constexpr int S = 8;                               // ring slots
+    // pointwise stage inputs (A and/or F) of a level: TMA boxes OX x OY x 5
+    static constexpr int NAF = (MODE == M_S2) ? 2 : (MODE == M_S3) ? 1 : 0;
+    static constexpr int SAF = NAF ? 2 : 0;                   // A/F level slots
+    static constexpr int AFB = 5 * OX * OY;                   // one array's box
+    static constexpr int S = NAF ? 6 : 8;                     // ring slots
     static constexpr int NXF = 6 * OY * TX, NYF = 6 * TY * OX;   // face partials per level
     static constexpr int DN = (N + 1) * (N + 1);
     static constexpr size_t SMEM =
-        sizeof(double) * ((size_t)S * SS + 2 * (NXF + NYF) + 2 * DN + OX + OY) + sizeof(uint64_t) * S + 128;
+        sizeof(double) * ((size_t)S * SS + (size_t)SAF * NAF * AFB + 2 * (NXF + NYF) + 2 * DN + OX + OY) +
+        sizeof(uint64_t) * (S + SAF) + 128;
     static constexpr uint32_t LVL_BYTES = (uint32_t)(sizeof(double) * 5 * PL);
     static constexpr uint32_t PP_BYTES = (uint32_t)(sizeof(double) * PL);
+    static constexpr uint32_t AF_BYTES = (uint32_t)(sizeof(double) * AFB);
     __host__ __device__ static constexpr int foff(int f) { return f < 5 ? f * PL : PPO; }
 };
 
@@ -184,10 +190,11 @@ __device__ __forceinline__ void ec_epilogue(const EArgs& a, const LvlTab& lt, lo
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(EC<N>::BLK, 1)
+__global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     k_ecol(const EArgs a, const __grid_constant__ LvlTab lt, const __grid_constant__ CUtensorMap tmq,
-           const __grid_constant__ CUtensorMap tmp) {
-    using T = EC<N>;
+           const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmA,
+           const __grid_constant__ CUtensorMap tmF) {
+    using T = EC<N, MODE>;
     constexpr int PL = T::PL, LXT = T::LXT, SS = T::SS, S = T::S, BLK = T::BLK;
     constexpr int OX = T::OX, OY = T::OY, TX = T::TX, TY = T::TY;
     constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
@@ -196,11 +203,12 @@ __global__ void __launch_bounds__(EC<N>::BLK, 1)
     extern __shared__ __align__(128) unsigned char smraw[];
     double* ring = reinterpret_cast<double*>(
         smraw + ((128u - ((unsigned)__cvta_generic_to_shared(smraw) & 127u)) & 127u));
-    double* XFb = ring + S * SS;          // [2][NXF]  XF[f][oy][j]
+    double* sAF = ring + S * SS;          // [SAF][NAF][5][OY][OX]: A (M_S2) | F
+    double* XFb = sAF + T::SAF * T::NAF * T::AFB;   // [2][NXF]  XF[f][oy][j]
     double* YFb = XFb + 2 * T::NXF;       // [2][NYF]  YF[f][j][ox]
     double* sD = YFb + 2 * T::NYF;        // Dx | Dy
     double* sC = sD + 2 * T::DN;          // cx of the tile's columns | cy of its rows
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(sC + OX + OY);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sC + OX + OY);   // [S] ring, [SAF] A/F
 
     const Geo& g = a.g;
     const int Z = g.Z;
@@ -212,7 +220,7 @@ __global__ void __launch_bounds__(EC<N>::BLK, 1)
     const int tx0 = (ex0 - 1) * N - g.x0, ty0 = (ey0 - 1) * N - g.y0;
 
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+        for (int s = 0; s < S + T::SAF; ++s) mbar_init(&mbar[s], 1);
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmq) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmp) : "memory");
     }
@@ -232,8 +240,23 @@ __global__ void __launch_bounds__(EC<N>::BLK, 1)
         tma_load_4d(slot, &tmq, bar, tx0, ty0, l, 0);
         tma_load_4d(slot + T::PPO, &tmp, bar, tx0, ty0, l, 0);
     };
+    // A/F boxes of a level (window-local origin of the owned tile)
+    const int ax0 = ex0 * N - g.x0, ay0 = ey0 * N - g.y0;
+    auto issue_af = [&](int l) {
+        if (T::NAF == 0) return;
+        double* dst = sAF + (l % T::SAF) * (T::NAF * T::AFB);
+        uint64_t* bar = &mbar[S + l % T::SAF];
+        mbar_expect_tx(bar, T::NAF * T::AF_BYTES);
+        if (MODE == M_S2) {
+            tma_load_4d(dst, &tmA, bar, ax0, ay0, l, 0);
+            tma_load_4d(dst + T::AFB, &tmF, bar, ax0, ay0, l, 0);
+        } else {
+            tma_load_4d(dst, &tmF, bar, ax0, ay0, l, 0);
+        }
+    };
     if (tid == 0) {
         for (int l = 0; l < S && l < Z; ++l) issue(l);
+        for (int l = 0; l < T::SAF && l < Z; ++l) issue_af(l);
     }
 
     // per-thread constants
@@ -341,14 +364,6 @@ __global__ void __launch_bounds__(EC<N>::BLK, 1)
             }
         }
         const long long o = colo + (long long)l * zs;
-        double Ai[5] = {0, 0, 0, 0, 0}, Fi[5] = {0, 0, 0, 0, 0};
-        if (own) {
-#pragma unroll
-            for (int f = 0; f < 5; ++f) {
-                if (MODE == M_S2) Ai[f] = a.A[o + f * fs];
-                if (MODE == M_S2 || MODE == M_S3) Fi[f] = a.F[o + f * fs];
-            }
-        }
         const double* slot = ring + (l % S) * SS;
         const double* xfb = XFb + (l & 1) * T::NXF;
         const double* yfb = YFb + (l & 1) * T::NYF;
@@ -401,6 +416,20 @@ __global__ void __launch_bounds__(EC<N>::BLK, 1)
         }
         if (own) {
             if (NEED_R) ec_check(a, p, lt.v[C_TH0][l]);
+            double Ai[5] = {0, 0, 0, 0, 0}, Fi[5] = {0, 0, 0, 0, 0};
+            if (T::NAF) {
+                mbar_wait(&mbar[S + l % T::SAF], (l / T::SAF) & 1);
+                const double* af = sAF + (l % T::SAF) * (T::NAF * T::AFB) + tid;
+#pragma unroll
+                for (int f = 0; f < 5; ++f) {
+                    if (MODE == M_S2) {
+                        Ai[f] = af[f * OX * OY];
+                        Fi[f] = af[T::AFB + f * OX * OY];
+                    } else {
+                        Fi[f] = af[f * OX * OY];
+                    }
+                }
+            }
             double Rv[5], Lv[5];
             ec_finish<MODE>(p, c, rho0, lt.v[C_DRHO0][l], lt.v[C_DTH0][l], lt.v[C_IRHO0][l], gr, bx, by,
                             (l == 0) || top, Rv, Lv);
@@ -408,10 +437,13 @@ __global__ void __launch_bounds__(EC<N>::BLK, 1)
         }
         if (l + 1 < Z) faces(l + 1, (l + 1) & 1);
         __syncthreads();
-        if (tid == 0 && l + S < Z) {
-            // generic-proxy reads of the slot are ordered before its async-proxy refill
+        // refills of the slots level l used; the issuing warp rotates so the
+        // issue latency does not always fall on the same warp
+        if (tid == 32 * (l % (BLK / 32)) && (l + S < Z || (T::NAF && l + T::SAF < Z))) {
+            // generic-proxy reads of the slots are ordered before their async-proxy refill
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(l + S);
+            if (l + S < Z) issue(l + S);
+            if (T::NAF && l + T::SAF < Z) issue_af(l + T::SAF);
         }
         if (!top) k = (k + 1 == N) ? 0 : k + 1;
     }

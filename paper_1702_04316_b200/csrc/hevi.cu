@@ -1515,17 +1515,21 @@ bool col_applies(const hevi_plan* pl, int mode, const EArgs& a) {
 
 template <int N, int MODE>
 int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
-    using T = EC<N>;
+    using T = EC<N, MODE>;
     const Geo& g = pl->g;
     static size_t attr[16] = {0};
     auto kern = k_ecol<N, MODE>;
     int rc = set_smem_attr(kern, T::SMEM, attr);
     if (rc) return rc;
-    CUtensorMap tq, tp;
+    CUtensorMap tq, tp, tA, tF;
     if ((rc = make_tmap(&tq, g, a.q, T::LXT, T::LY, 1))) return rc;
     if ((rc = make_tmap(&tp, g, a.pp_in, T::LXT, T::LY, 1, 1))) return rc;
+    tA = tq;
+    tF = tq;
+    if (MODE == M_S2 && (rc = make_tmap(&tA, g, a.A, T::OX, T::OY, 1))) return rc;
+    if ((MODE == M_S2 || MODE == M_S3) && (rc = make_tmap(&tF, g, a.F, T::OX, T::OY, 1))) return rc;
     const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
-    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp);
+    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF);
     CK(cudaGetLastError());
     // domain-end planes owned by this rank
     const int nxc = (g.ex_e == g.nex) ? (g.ey_e - g.ey_b) * N + (g.ey_e == g.ney ? 1 : 0) : 0;
