@@ -31,14 +31,19 @@
 // parameter block: warp-uniform indices, no shared-memory bandwidth.
 #pragma once
 
-#define EC_ZMAX 96
+#define EC_ZMAX 64
+#define EC_NMAX 4
 enum { C_RHO0 = 0, C_TH0, C_DRHO0, C_DTH0, C_CZ, C_IRHO0, C_G0, C_H0, C_PB, C_C0, C_IRT0, C_P0F, EC_NT };
 
+// per-level constants of the explicit_col kernels (N <= EC_NMAX, Z <= EC_ZMAX);
+// row(l) = l mod N (N on the top level), base(l) = l - row(l)
 struct LvlTab {
     double v[EC_NT][EC_ZMAX];
-    double dx[81], dy[81], dz[81];   // (N+1)^2 derivative matrices, row-major
-    double dzs[EC_ZMAX][9];          // cz[l] * Dz[row(l)][m]: the level's scaled vertical D row
+    double dx[25], dy[25], dz[25];   // (N+1)^2 derivative matrices, row-major
+    double dzs[EC_ZMAX][5];          // cz[l] * Dz[row(l)][m]: the level's scaled vertical D row
     double czf[EC_ZMAX];             // cz[l] on a bottom element face (carry from below), else 0
+    double pg[EC_ZMAX][5], ph[EC_ZMAX][5];   // dzs[l][m] * G0 / H0 [base(l) + m]: d/dz of P_lin
+    double cg[EC_ZMAX][5], ch[EC_ZMAX][5];   // Dz[N][m] * G0 / H0 [l + m]: row-N carry of P_lin, layer base l
 };
 
 template <int N, int MODE>

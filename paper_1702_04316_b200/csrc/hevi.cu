@@ -1211,6 +1211,10 @@ struct hevi_plan {
     bool use_tma = true;
     bool use_col = true;     // explicit_col kernels (3D, N = 4, set2nc)
     bool lt_ok = false;      // lt filled (Z <= EC_ZMAX)
+    // fork/join of the domain-end kernel (k_ecol_edge) beside the main sweep:
+    // it runs in the main kernel's last, partial wave (capturable in graphs)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     LvlTab lt;               // per-level constants of the explicit_col kernels
 };
 
@@ -1528,17 +1532,26 @@ int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     tF = tq;
     if (MODE == M_S2 && (rc = make_tmap(&tA, g, a.A, T::OX, T::OY, 1))) return rc;
     if ((MODE == M_S2 || MODE == M_S3) && (rc = make_tmap(&tF, g, a.F, T::OX, T::OY, 1))) return rc;
-    const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
-    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF);
-    CK(cudaGetLastError());
     // domain-end planes owned by this rank
     const int nxc = (g.ex_e == g.nex) ? (g.ey_e - g.ey_b) * N + (g.ey_e == g.ney ? 1 : 0) : 0;
     const int nyr = (g.ey_e == g.ney) ? (g.ex_e - g.ex_b) * N : 0;
     const long long npt = (long long)(nxc + nyr) * g.Z;
+    const bool fork = npt > 0 && pl->side != nullptr;
+    if (fork) CK(cudaEventRecord(pl->ev_fork, st));
+    const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
+    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF);
+    CK(cudaGetLastError());
     if (npt > 0) {
-        k_ecol_edge<N, MODE><<<(unsigned)((npt + 127) / 128), 128, 0, st>>>(a, pl->lt, nxc, nyr, g.ex_b * N,
+        // launched after the sweep: its blocks are dispatched as the sweep's last CTAs retire
+        cudaStream_t es = fork ? pl->side : st;
+        if (fork) CK(cudaStreamWaitEvent(es, pl->ev_fork, 0));
+        k_ecol_edge<N, MODE><<<(unsigned)((npt + 127) / 128), 128, 0, es>>>(a, pl->lt, nxc, nyr, g.ex_b * N,
                                                                           g.ey_b * N);
         CK(cudaGetLastError());
+        if (fork) {
+            CK(cudaEventRecord(pl->ev_join, es));
+            CK(cudaStreamWaitEvent(st, pl->ev_join, 0));
+        }
     }
     return HEVI_OK;
 }
@@ -1862,6 +1875,11 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     if (e == cudaSuccess) e = cudaMalloc(&pl->d_flags, 16 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(pl->d_flags, 0, 16 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMallocHost(&pl->h_flags, 16 * sizeof(unsigned));
+    if (e == cudaSuccess && getenv("HEVI_NO_FORK") == nullptr) {
+        e = cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming);
+    }
 #ifdef HEVI_PHASE_TIMING
     if (e == cudaSuccess) e = cudaMalloc(&pl->d_dbg, 8 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(pl->d_dbg, 0, 8 * sizeof(unsigned long long));
@@ -1893,7 +1911,7 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     pl->use_v2 = getenv("HEVI_KERNELS") == nullptr || strcmp(getenv("HEVI_KERNELS"), "v1") != 0;
     pl->use_tma = getenv("HEVI_NO_TMA") == nullptr;
     pl->use_col = pl->use_v2 && (getenv("HEVI_KERNELS") == nullptr || strcmp(getenv("HEVI_KERNELS"), "v2") != 0);
-    if (Z <= EC_ZMAX && nd <= 81 && ndy <= 81) {
+    if (Z <= EC_ZMAX && gd->N <= EC_NMAX && gd->Ny == gd->N) {
         LvlTab& t = pl->lt;
         memset(&t, 0, sizeof(t));
         for (int k = 0; k < Z; ++k) {
@@ -1916,7 +1934,16 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
         const int N = gd->N;
         for (int k = 0; k < Z; ++k) {
             const int row = (k == Z - 1) ? N : k % N;
-            for (int m = 0; m <= N; ++m) t.dzs[k][m] = rd->cz[k] * rd->Dz[row * (N + 1) + m];
+            const int base = k - row;
+            for (int m = 0; m <= N; ++m) {
+                t.dzs[k][m] = rd->cz[k] * rd->Dz[row * (N + 1) + m];
+                t.pg[k][m] = t.dzs[k][m] * rd->G0[base + m];
+                t.ph[k][m] = t.dzs[k][m] * rd->H0[base + m];
+                if (k + m < Z) {
+                    t.cg[k][m] = rd->Dz[N * (N + 1) + m] * rd->G0[k + m];
+                    t.ch[k][m] = rd->Dz[N * (N + 1) + m] * rd->H0[k + m];
+                }
+            }
             t.czf[k] = (row == 0 && k > 0) ? rd->cz[k] : 0.0;
         }
         pl->lt_ok = true;
@@ -1941,6 +1968,9 @@ int hevi_plan_destroy(hevi_plan* pl) {
         cudaFree(kv.second.piv);
         cudaFree(kv.second.d_info);
     }
+    if (pl->side) cudaStreamDestroy(pl->side);
+    if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
+    if (pl->ev_join) cudaEventDestroy(pl->ev_join);
     cudaFree(pl->d_tab);
     cudaFree(pl->d_flags);
     if (pl->h_flags) cudaFreeHost(pl->h_flags);
