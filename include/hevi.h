@@ -130,6 +130,13 @@ int hevi_rk35_step(hevi_plan *plan, double dt, double *Q, double *work, void *st
  * the first-occurrence copy, columnsolve.unique_space rep :28-34) */
 int hevi_evec_to_lattice(hevi_plan *plan, const double *E, double *Lat, int nfields, void *stream);
 int hevi_lattice_to_evec(hevi_plan *plan, const double *Lat, double *E, int nfields, void *stream);
+/* specgrid.apply_dss / apply_dss_many (specgrid.py:535-548) on E-vectors
+ * (nfields stacked): every coincident node copy <- sum_c w_c f_c / sum_c w_c,
+ * w = wJ per node as the product of per-axis tables wx[kx*(N+1)+i] (GLL
+ * weight x half element width), wy, wz (device arrays).  Whole-domain
+ * plans only; Ein and Eout must not alias. */
+int hevi_dss(hevi_plan *plan, const double *Ein, double *Eout, int nfields, const double *wx,
+             const double *wy, const double *wz, void *stream);
 
 /* sticky device flags: OR of HEVI_F_* since the last reset (synchronises stream) */
 int hevi_flags(hevi_plan *plan, unsigned *flags, int reset, void *stream);
@@ -159,6 +166,13 @@ int hevi_flags(hevi_plan *plan, unsigned *flags, int reset, void *stream);
  * deterministic order);
  * hevi_axpby: y = alpha x + beta y over n doubles. */
 int hevi_linear3(hevi_plan *plan, const double *q, double *out, void *stream);
+/* Discretization.gradc / grad_vc (euler.py:281-295): out (3 lattice fields)
+ * = DSS-projected gradient of the scalar lattice field f; vertical_only = 1
+ * gives grad_vc (x, y components zero on a box, vert = z) */
+int hevi_grad(hevi_plan *plan, int vertical_only, const double *f, double *out, void *stream);
+/* Discretization.divc / div_vc (euler.py:287-300): out = DSS-projected
+ * divergence of the 3-field lattice vector vec (vertical_only: d/dz of vec_z) */
+int hevi_div(hevi_plan *plan, int vertical_only, const double *vec, double *out, void *stream);
 int hevi_schur3_up(hevi_plan *plan, double lam, int vertical_only, const double *P, double *up,
                    void *stream);
 int hevi_schur3_flux(hevi_plan *plan, double lam, int vertical_only, const double *P,

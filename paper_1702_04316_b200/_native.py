@@ -80,6 +80,9 @@ SIGNATURES = {
     "hevi_halo_pack": (_I, [_V, _V, _I, _I, _I, _I, _I, _V, _V]),
     "hevi_halo_unpack": (_I, [_V, _V, _I, _I, _I, _I, _I, _V, _V]),
     "hevi_linear3": (_I, [_V, _V, _V, _V]),
+    "hevi_grad": (_I, [_V, _I, _V, _V, _V]),
+    "hevi_div": (_I, [_V, _I, _V, _V, _V]),
+    "hevi_dss": (_I, [_V, _V, _V, _I, _V, _V, _V, _V]),
     "hevi_schur3_up": (_I, [_V, _D, _I, _V, _V, _V]),
     "hevi_schur3_flux": (_I, [_V, _D, _I, _V, _V, _V, _V]),
     "hevi_schur3_ua": (_I, [_V, _D, _V, _V, _V, _V]),

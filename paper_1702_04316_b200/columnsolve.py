@@ -82,6 +82,48 @@ class ColumnJacobian:
         return self.matrices.shape[1]
 
 
+def _unique_apply(problem, space: UniqueSpace, n_dof: int):
+    """Vertical LHS as an operator on (n_col, n_lev, n_dof) unique values
+    (columnsolve.py:52-72), Schur form: the values are laid on the lattice
+    (unique (column, level) points), lhs_schur runs on the device
+    (hevi_schur3_up + hevi_schur3_flux, vertical-only derivatives)."""
+    import torch
+    if n_dof != 1:
+        raise NotImplementedError("the device path implements the Schur (pressure) form")
+    mesh = problem.disc.mesh
+    plan = problem.disc.plan_for(problem.ref, problem.set_name)
+    Z, Y, X = mesh.Z, mesh.Y, mesh.X
+
+    def apply_u(U):
+        Ut = torch.as_tensor(np.asarray(U) if not isinstance(U, torch.Tensor) else U,
+                             dtype=torch.float64, device=plan.device).reshape(space.n_col, space.n_lev)
+        if mesh.slab:
+            P = Ut.t()[:, None, :].expand(Z, Y, X)
+        else:
+            P = Ut.t().reshape(Z, Y, X)
+        L = plan.padded(P[None].contiguous())
+        lam = float(problem.lam)
+        up = plan.schur3_up(lam, L[0], plan.zeros(3), True)
+        out = plan.schur3_flux(lam, L[0], up, plan.zeros(1)[0], True)
+        O = out[:, :, :X]
+        O = O[:, 0, :] if mesh.slab else O.reshape(Z, Y * X)
+        res = O.t().reshape(space.n_col, space.n_lev, 1)
+        return res if isinstance(U, torch.Tensor) else res.cpu().numpy()
+    return apply_u
+
+
+def _leakage_check(problem, space):
+    """Probing one column must not touch any other (columnsolve.py:94-101)."""
+    import torch
+    apply_u = _unique_apply(problem, space, 1)
+    U = torch.zeros((space.n_col, space.n_lev, 1), dtype=torch.float64, device="cuda")
+    U[0, space.n_lev // 2, 0] = 1.0
+    out = apply_u(U)
+    if float(out[1:].abs().max()) > 1e-13 * max(1.0, float(out[0].abs().max())):
+        raise RuntimeError("cross-column leakage detected in the vertical operator; "
+                           "columns are not independent")
+
+
 def build_column_jacobian(problem) -> ColumnJacobian:
     """Probe the Schur column operator (columnsolve.py:75-108) on the device.
 
@@ -101,6 +143,7 @@ def build_column_jacobian(problem) -> ColumnJacobian:
     else:
         A, _ = plan.column_matrix(lam)
         nb = plan.factor(lam)
+        _leakage_check(problem, space)
     mats = torch.as_tensor(A, device=plan.device).expand(space.n_col, -1, -1).contiguous()
     return ColumnJacobian(matrices=mats, bandwidth=nb, n_dof=1, space=space,
                           pivoted_fallback=[], piv={})

@@ -59,6 +59,7 @@ struct EC {
     // pointwise stage inputs (A and/or F) of a level: TMA boxes OX x OY x 5
     static constexpr int NAF = (MODE == M_S2) ? 2 : (MODE == M_S3) ? 1 : 0;
     static constexpr int SAF = NAF ? 2 : 0;                   // A/F level slots
+    static constexpr int SAFM = NAF ? SAF : 1;                // (modulus when SAF is 0)
     static constexpr int AFB = 5 * OX * OY;                   // one array's box
     static constexpr int S = NAF ? 6 : 8;                     // ring slots
     static constexpr int NXF = 6 * OY * TX, NYF = 6 * TY * OX;   // face partials per level
@@ -249,8 +250,8 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     const int ax0 = ex0 * N - g.x0, ay0 = ey0 * N - g.y0;
     auto issue_af = [&](int l) {
         if (T::NAF == 0) return;
-        double* dst = sAF + (l % T::SAF) * (T::NAF * T::AFB);
-        uint64_t* bar = &mbar[S + l % T::SAF];
+        double* dst = sAF + (l % T::SAFM) * (T::NAF * T::AFB);
+        uint64_t* bar = &mbar[S + l % T::SAFM];
         mbar_expect_tx(bar, T::NAF * T::AF_BYTES);
         if (MODE == M_S2) {
             tma_load_4d(dst, &tmA, bar, ax0, ay0, l, 0);
@@ -284,7 +285,6 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     const int yfo = (oy / N) * OX + ox;
     const long long colo = (long long)(gy - g.y0) * g.px + (gx - g.x0);
     const long long zs = (long long)g.lY * g.px;
-    const long long fs = g.fs;
     const double gr = a.ph.g;
 
     // element-face partials (row N of the left / lower element) of level l
@@ -340,7 +340,6 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     int k = 0;
     for (int l = 0; l < Z; ++l) {
         const bool top = (l == Z - 1);
-        const int krow = top ? N : k;
         if (k == 0 && !top) {
             if (l > 0) {
                 // carries of the finished layer (row N of its element)
@@ -378,7 +377,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
         const double czf = lt.czf[l];
         const double rho0 = lt.v[C_RHO0][l];
 
-        // the point's own state (level krow of the window, read from its slot)
+        // the point's own state (its window level is dynamic: read from the slot)
         PtSt p;
         p.r = slot[po];
         p.u = slot[PL + po];
@@ -423,8 +422,8 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
             if (NEED_R) ec_check(a, p, lt.v[C_TH0][l]);
             double Ai[5] = {0, 0, 0, 0, 0}, Fi[5] = {0, 0, 0, 0, 0};
             if (T::NAF) {
-                mbar_wait(&mbar[S + l % T::SAF], (l / T::SAF) & 1);
-                const double* af = sAF + (l % T::SAF) * (T::NAF * T::AFB) + tid;
+                mbar_wait(&mbar[S + l % T::SAFM], (l / T::SAFM) & 1);
+                const double* af = sAF + (l % T::SAFM) * (T::NAF * T::AFB) + tid;
 #pragma unroll
                 for (int f = 0; f < 5; ++f) {
                     if (MODE == M_S2) {

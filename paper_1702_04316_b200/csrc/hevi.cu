@@ -989,6 +989,65 @@ __global__ void k_l2e(const double* Lt, double* E, const CArgs a, int nf) {
     }
 }
 
+// specgrid.apply_dss (specgrid.py:535-540) on E-vectors: every coincident
+// copy of a lattice point takes the mass-weighted average of all copies,
+// sum_c w_c f_c / sum_c w_c, summed in the reference's flat node order
+// (elements in (kz, ky, kx) order, the lower element first on a face).
+// w_c = Wx[kx][i] Wy[ky][j] Wz[kz][k] (quadrature weight x half element
+// width per axis: the box mesh's wJ).  One thread per lattice point, no
+// atomics; any discontinuous E-vector is accepted.
+__global__ void k_dss(const double* __restrict__ Ein, double* __restrict__ Eout, const CArgs a, int nf,
+                      const double* __restrict__ Wx, const double* __restrict__ Wy,
+                      const double* __restrict__ Wz) {
+    const Geo& g = a.g;
+    const int X = g.X, Y = g.Y, Zl = g.Z;
+    const long long n = (long long)X * Y * Zl;
+    const int nr = a.N + 1, ns = a.Ny + 1, nt = a.N + 1;
+    const long long npe = (long long)nr * ns * nt;
+    const long long fsE = a.nel * npe;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int gx = idx % X;
+        const long long t = idx / X;
+        const int gy = t % Y;
+        const int gz = t / Y;
+        int ex[2], ix[2], ey[2], iy[2], ez[2], iz[2];
+        auto copies = [](int gi, int N, int ne, int* e, int* l) {
+            if (gi > 0 && gi < ne * N && gi % N == 0) {
+                e[0] = gi / N - 1; l[0] = N;
+                e[1] = gi / N;     l[1] = 0;
+                return 2;
+            }
+            e[0] = min(gi / N, ne - 1);
+            l[0] = gi - e[0] * N;
+            return 1;
+        };
+        const int cx = copies(gx, a.N, g.nex, ex, ix);
+        const int cy = copies(gy, a.Ny, g.ney, ey, iy);
+        const int cz = copies(gz, a.N, g.nez, ez, iz);
+        for (int f = 0; f < nf; ++f) {
+            double num = 0.0, den = 0.0;
+            for (int c3 = 0; c3 < cz; ++c3)
+                for (int c2 = 0; c2 < cy; ++c2)
+                    for (int c1 = 0; c1 < cx; ++c1) {
+                        const long long e = ((long long)ez[c3] * g.ney + ey[c2]) * g.nex + ex[c1];
+                        const long long node = e * npe + ((long long)iz[c3] * ns + iy[c2]) * nr + ix[c1];
+                        const double w = (Wx[ex[c1] * nr + ix[c1]] * Wy[ey[c2] * ns + iy[c2]]) *
+                                         Wz[ez[c3] * nt + iz[c3]];
+                        num += w * Ein[f * fsE + node];
+                        den += w;
+                    }
+            const double v = num / den;
+            for (int c3 = 0; c3 < cz; ++c3)
+                for (int c2 = 0; c2 < cy; ++c2)
+                    for (int c1 = 0; c1 < cx; ++c1) {
+                        const long long e = ((long long)ez[c3] * g.ney + ey[c2]) * g.nex + ex[c1];
+                        Eout[f * fsE + e * npe + ((long long)iz[c3] * ns + iy[c2]) * nr + ix[c1]] = v;
+                    }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // generic batched banded column API
 // ---------------------------------------------------------------------------
@@ -2267,6 +2326,22 @@ int hevi_evec_to_lattice(hevi_plan* pl, const double* E, double* Lt, int nf, voi
     return HEVI_OK;
 }
 
+int hevi_dss(hevi_plan* pl, const double* Ein, double* Eout, int nf, const double* wx, const double* wy,
+             const double* wz, void* stream) {
+    if (!pl || !Ein || !Eout || !wx || !wy || !wz) return fail("null argument");
+    if (pl->g.lX != pl->g.X || pl->g.lY != pl->g.Y) return fail("hevi_dss needs a whole-domain plan");
+    if (Ein == Eout) return fail("hevi_dss: input and output must not alias");
+    CArgs a;
+    a.g = pl->g;
+    a.N = pl->N;
+    a.Ny = pl->Ny;
+    a.nel = (long long)pl->g.nex * pl->g.ney * pl->g.nez;
+    const long long n = (long long)pl->g.X * pl->g.Y * pl->g.Z;
+    k_dss<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(Ein, Eout, a, nf, wx, wy, wz);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
 int hevi_lattice_to_evec(hevi_plan* pl, const double* Lt, double* E, int nf, void* stream) {
     if (!pl || !E || !Lt) return fail("null argument");
     if (pl->g.lX != pl->g.X || pl->g.lY != pl->g.Y) return fail("lattice_to_evec needs the full lattice");
@@ -2360,6 +2435,24 @@ static int i3blocks(const hevi_plan* pl) {
 int hevi_linear3(hevi_plan* pl, const double* q, double* out, void* stream) {
     if (!pl || !q || !out) return fail("null argument");
     k3_linear<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(i3args(pl, 0.0), q, out);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_grad(hevi_plan* pl, int vertical_only, const double* f, double* out, void* stream) {
+    if (!pl || !f || !out) return fail("null argument");
+    I3Args a = i3args(pl, 0.0);
+    a.vert_only = vertical_only ? 1 : 0;
+    k3_grad<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(a, f, out);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_div(hevi_plan* pl, int vertical_only, const double* vec, double* out, void* stream) {
+    if (!pl || !vec || !out) return fail("null argument");
+    I3Args a = i3args(pl, 0.0);
+    a.vert_only = vertical_only ? 1 : 0;
+    k3_div<<<i3blocks(pl), 256, 0, (cudaStream_t)stream>>>(a, vec, out);
     CK(cudaGetLastError());
     return HEVI_OK;
 }

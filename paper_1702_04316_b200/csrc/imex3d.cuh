@@ -282,6 +282,34 @@ __global__ void k3_extract(const I3Args a, const double* __restrict__ P, const d
     }
 }
 
+// DSS-projected gradient of a scalar (Discretization.gradc / grad_vc,
+// euler.py:281-295): out = (d/dx, d/dy, d/dz) f, three fields; with
+// vert_only the x, y components are zero (grad_vc multiplies the vertical
+// derivative by vert = z on a box)
+__global__ void k3_grad(const I3Args a, const double* __restrict__ f, double* __restrict__ out) {
+    const Geo& g = a.g;
+    const long long n = (long long)g.Z * g.lY * g.lX;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const P3 p = point3(g, i);
+    double gx, gy, gz;
+    grad3(a, p, [&](long long o, int) { return __ldg(f + o); }, gx, gy, gz);
+    out[p.o] = gx;
+    out[p.o + g.fs] = gy;
+    out[p.o + 2 * g.fs] = gz;
+}
+
+// DSS-projected divergence of a 3-field vector (Discretization.divc /
+// div_vc, euler.py:287-300)
+__global__ void k3_div(const I3Args a, const double* __restrict__ vec, double* __restrict__ out) {
+    const Geo& g = a.g;
+    const long long n = (long long)g.Z * g.lY * g.lX;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const P3 p = point3(g, i);
+    out[p.o] = div3(a, p, vec);
+}
+
 // ---- Krylov vector kernels -------------------------------------------------
 constexpr int KV_BLOCKS = 296, KV_T = 256;
 

@@ -210,6 +210,115 @@ class ImplicitProblem:
         return out
 
 
+    # -- operator pieces of the reference object (imexcore.py:190-298) ----------
+    # E-vectors in and out (numpy or torch); the arithmetic runs in the
+    # library's lattice kernels (hevi_schur3_*, hevi_linear_v / hevi_linear3,
+    # hevi_grad / hevi_div), with the vertical-only derivatives when dim="1d".
+    def _plan(self):
+        euler._check_set(self.set_name, self.discretization == "dg")
+        return self.disc.plan_for(self.ref, self.set_name)
+
+    @staticmethod
+    def _vec_in(plan, v):
+        """(..., 3) E-vector -> (3, Z, lY, px) lattice tensor, and the way back."""
+        from .plan import to_device
+        E, back = to_device(v)
+        return plan.e2l(E.movedim(-1, 0).contiguous()), (lambda L: back(plan.l2e(L).movedim(0, -1).contiguous()))
+
+    @staticmethod
+    def _scalar_in(plan, f):
+        from .plan import to_device
+        E, back = to_device(f)
+        return plan.e2l(E[None].contiguous()), (lambda L: back(plan.l2e(L)[0]))
+
+    def lhs_standard(self, q):
+        """(I - lam L) q in the 5-variable standard form (imexcore.py:196-198)."""
+        plan = self._plan()
+        Q, back = plan.lattice_in(q)
+        L = plan.linear(Q, plan.zeros()) if self.dim == "1d" else plan.linear3(Q, plan.zeros())
+        plan.check_flags()
+        plan.axpby(-float(self.lam), L, 1.0, Q)
+        return back(Q)
+
+    def _ainv(self, v):
+        """Rank-one (Sherman-Morrison) inverse of A = I + lam^2 u w^T
+        (imexcore.py:200-217); u, w are vertical on a box, so only the z
+        component changes."""
+        import torch
+        from .plan import to_device
+        ref = self.ref
+        w = ref.dtheta0      # grad theta0 (set2nc) = grad G0_c (set2c), vertical
+        if not np.any(w):
+            return v
+        E, back = to_device(v)
+        dev = E.device
+        node = lambda a: torch.as_tensor(ref.node(a), device=dev)  # noqa: E731
+        u = (self.lam ** 2 / node(ref.theta0)) * ref.const.g
+        den = 1.0 + node(w) * u
+        if bool((den.abs() < 1e-12).any()):
+            raise FloatingPointError("rank-one inverse denominator underflow")
+        out = E.clone()
+        out[..., 2] = E[..., 2] - u * ((node(w) * E[..., 2]) / den)
+        return back(out)
+
+    def _gradP(self, P):
+        return self.disc.grad_vc(P) if self.dim == "1d" else self.disc.gradc(P)
+
+    def _div(self, vec):
+        return self.disc.div_vc(vec) if self.dim == "1d" else self.disc.divc(vec)
+
+    def rhs_schur_build(self, q_e):
+        """Pressure right-hand side and the stored velocity-like estimate
+        (imexcore.py:229-243): (rhs, ua) with ua of shape (..., 3)."""
+        plan = self._plan()
+        lam = float(self.lam)
+        Qe, _ = plan.lattice_in(q_e)
+        ua = plan.zeros(3)
+        Pe = plan.zeros(1)[0]
+        plan.schur3_ua(lam, Qe, ua, Pe)
+        rhs = plan.schur3_flux(lam, Pe, ua, plan.zeros(1)[0], self.dim == "1d")
+        plan.check_flags()
+        E = plan.l2e(rhs[None])[0]
+        U = plan.l2e(ua).movedim(0, -1).contiguous()
+        return _back_like(q_e, E), _back_like(q_e, U)
+
+    def _up(self, P):
+        """Pressure-driven velocity-like variable (imexcore.py:245-257), (..., 3)."""
+        plan = self._plan()
+        L, _ = self._scalar_in(plan, P)
+        up = plan.schur3_up(float(self.lam), L[0], plan.zeros(3), self.dim == "1d")
+        plan.check_flags()
+        return _back_like(P, plan.l2e(up).movedim(0, -1).contiguous())
+
+    def _helmholtz_flux(self, vel):
+        """lam-scaled pressure-equation flux of a velocity-like field (imexcore.py:259-268)."""
+        plan = self._plan()
+        V, _ = self._vec_in(plan, vel)
+        neg = plan.schur3_flux(float(self.lam), plan.zeros(1)[0], V, plan.zeros(1)[0], self.dim == "1d")
+        return _back_like(vel, -plan.l2e(neg[None])[0])
+
+    def lhs_schur(self, P):
+        """P - helmholtz_flux(up(P)) (imexcore.py:270-271)."""
+        plan = self._plan()
+        L, _ = self._scalar_in(plan, P)
+        lam, vo = float(self.lam), self.dim == "1d"
+        up = plan.schur3_up(lam, L[0], plan.zeros(3), vo)
+        out = plan.schur3_flux(lam, L[0], up, plan.zeros(1)[0], vo)
+        plan.check_flags()
+        return _back_like(P, plan.l2e(out[None])[0])
+
+    def extract_from_pressure(self, P, ua, q_e):
+        """q from the solved pressure, the estimate ua and q_e (imexcore.py:273-298)."""
+        plan = self._plan()
+        lam, vo = float(self.lam), self.dim == "1d"
+        L, _ = self._scalar_in(plan, P)
+        U, _ = self._vec_in(plan, ua)
+        Qe, back = plan.lattice_in(q_e)
+        up = plan.schur3_up(lam, L[0], plan.zeros(3), vo)
+        q = plan.schur3_extract(lam, L[0], U, up, Qe, plan.zeros())
+        plan.check_flags()
+        return back(q)
+
     # -- 3D-IMEX Schur form (imexcore.py:229-298, 324-373) ----------------------
     def _krylov_path(self):
         if self.discretization != "cg":
@@ -317,6 +426,13 @@ class ImplicitProblem:
                                         precon=pre, x0=x0)
         return krylov.richardson_pbno(amap, b, tol=spec.tol, max_iter=spec.max_iter,
                                       precon=pre, x0=x0, check_every=spec.check_every)
+
+
+def _back_like(like, t):
+    """A device result in the array type of ``like`` (numpy -> numpy)."""
+    if isinstance(like, np.ndarray):
+        return t.cpu().numpy()
+    return t.to(like.device) if hasattr(like, "device") else t
 
 
 def _node_levels(mesh):

@@ -239,3 +239,76 @@ def build_box_mesh_3d(nx: int, ny: int, nz: int, Lx: float, Ly: float, Lz: float
     return BoxMesh(kind="box", N=N, Ny=N, nx=nx, ny=ny, nz=nz, Lx=Lx, Ly=Ly, Lz=Lz,
                    slab=False, quad_r=q, quad_s=q, quad_t=q,
                    meta={"nx": nx, "ny": ny, "nz": nz, "Lx": Lx, "Ly": Ly, "Lz": Lz})
+
+
+# ---------------------------------------------------------------------------
+# Direct stiffness summation on E-vectors (specgrid.py:512-548)
+# ---------------------------------------------------------------------------
+@dataclass
+class BoxDss:
+    """The DssMap of a box mesh (specgrid.py:512-532): the per-node mass
+    weight wJ = w_r w_s w_t J factors into one table per axis (GLL weight x
+    half element width), so the map is three short tables instead of an
+    E-vector sized group index.  ``plan`` returns a whole-domain device plan
+    of the mesh (the kernel only needs its geometry)."""
+    mesh: BoxMesh
+    wx: np.ndarray
+    wy: np.ndarray
+    wz: np.ndarray
+    plan: object = None
+    _dev: dict = field(default_factory=dict)
+
+    @property
+    def shape(self):
+        return tuple(self.mesh.nshape)
+
+    @property
+    def n_groups(self) -> int:
+        return self.mesh.n_unique
+
+    def device_tables(self, device):
+        key = str(device)
+        if key not in self._dev:
+            import torch
+            self._dev[key] = tuple(torch.as_tensor(w, dtype=torch.float64, device=device)
+                                   for w in (self.wx, self.wy, self.wz))
+        return self._dev[key]
+
+
+def build_dss_map(mesh: BoxMesh, plan_getter=None) -> BoxDss:
+    xe, ye, ze = mesh.edges()
+
+    def table(e, q, ne):
+        h = np.diff(e) if len(e) == ne + 1 else np.full(ne, e[-1] - e[0])
+        return (q.weights[None, :] * (0.5 * h)[:, None]).ravel()
+    if mesh.slab:
+        wy = mesh.quad_s.weights * (0.5 * mesh.Ly)
+    else:
+        wy = table(ye, mesh.quad_s, mesh.ny)
+    return BoxDss(mesh=mesh, wx=table(xe, mesh.quad_r, mesh.nx), wy=wy,
+                  wz=table(ze, mesh.quad_t, mesh.nz), plan=plan_getter)
+
+
+def apply_dss_many(fields, dss: BoxDss):
+    """DSS along the leading axis of stacked E-vector fields (specgrid.py:543-548):
+    every coincident copy takes the mass-weighted average of all copies, on
+    the device (``hevi_dss``).  numpy in -> numpy out, torch in -> torch out."""
+    from . import _native as nv
+    from .plan import to_device
+    import torch
+    E, back = to_device(fields)
+    if tuple(E.shape[1:]) != dss.shape:
+        raise ValueError("field/DSS map shape mismatch")
+    plan = dss.plan()
+    out = torch.empty_like(E)
+    wx, wy, wz = dss.device_tables(E.device)
+    nv.check(plan.lib.hevi_dss(plan.h, nv.ptr(E), nv.ptr(out), E.shape[0], nv.ptr(wx), nv.ptr(wy),
+                               nv.ptr(wz), nv.stream_ptr()))
+    return back(out)
+
+
+def apply_dss(f, dss: BoxDss):
+    """Replace coincident-node values by their mass-weighted average (specgrid.py:535-540)."""
+    if tuple(f.shape) != dss.shape:
+        raise ValueError("field/DSS map shape mismatch")
+    return apply_dss_many(f[None], dss)[0]

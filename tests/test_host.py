@@ -302,3 +302,121 @@ def test_rk35_generic_third_order_and_nan():
     assert 2.7 < math.log2(err(0.1) / err(0.05)) < 3.3
     with pytest.raises(FloatingPointError):
         imexcore.rk35_step(np.array([1.0]), 1.0, lambda x: x * np.nan)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "straka100"])
+def test_baseline_inputs_match_reference(name):
+    """The bench's synthetic inputs at the BASELINE configs are the
+    reference's: bubble IC (bench.py:108-124, harness 3D extension) and the
+    Courant dt rule (cli.py:187-194), against tests/golden/<name>.npz."""
+    import torch
+    from test_gpu_baseline_parity import BASE, build
+    from paper_1702_04316_b200 import cases
+    from conftest import load_golden
+    mesh, ref, disc = build(name)
+    g = load_golden(name)
+    b = BASE[name]
+    q0 = cases.bubble_lattice(mesh, ref, *b["bubble"], device="cpu")
+    want = g["step_q0"]
+    assert np.abs(q0.numpy() - want).max() <= 1e-14 * max(np.abs(want).max(), 1.0)
+    dt = cases.dt_for_courant(mesh, ref, q0, b["C"])
+    assert dt == pytest.approx(float(g["step_dt"]), rel=1e-12)
+    assert torch.isfinite(q0).all()
+
+
+def test_rounding_floor_file_covers_the_baseline_goldens():
+    """tests/golden/floor.json (make_baseline_golden.py) holds the reference's
+    same-host rounding floor for every kept step of every baseline golden."""
+    import json
+    from conftest import GOLDEN, load_golden
+    fl = json.load(open(os.path.join(GOLDEN, "floor.json")))
+    for name in ("cfg1", "cfg2", "straka100"):
+        g = load_golden(name)
+        keep = sorted(int(k[6:]) for k in g.files if k.startswith("step_q") and k != "step_q0")
+        for k in keep:
+            f = fl[name][str(k)]
+            assert 0.0 < f["vel"] < 1e-6 and f["rho"] < 1e-9 and f["theta"] < 1e-12, (name, k, f)
+
+
+# --- reference test_imexcore.py:93-158, 368-374: the stepper's duck-typed
+# problem protocol (a scalar problem solved exactly, no device operators) ---
+class ScalarProblem:
+    """q' = k q treated implicitly; exact scalar solve (test_imexcore.py:93-106)."""
+
+    def __init__(self, k_lin):
+        self.k = k_lin
+        self.lam = 0.0
+
+    def linear(self, q):
+        return np.zeros_like(q) if self.k == 0.0 else self.k * q
+
+    def solve(self, q_e):
+        return q_e / (1.0 - self.lam * self.k)
+
+
+def _explicit_rk(q, dt, a, b, rhs):
+    k = []
+    for i in range(len(b)):
+        qi = q.copy()
+        for j in range(i):
+            qi = qi + dt * a[i, j] * k[j]
+        k.append(rhs(qi))
+    out = q.copy()
+    for i in range(len(b)):
+        out = out + dt * b[i] * k[i]
+    return out
+
+
+def test_ark2_reduces_to_explicit_rk_when_linear_zero():
+    t = imexcore.ark2_tableau()
+    rhs = lambda q: np.sin(q) - 0.3 * q  # noqa: E731
+    q = np.array([0.7])
+    got = imexcore.ark_imex_step(q, 0.2, t, ScalarProblem(0.0), rhs)
+    assert np.array_equal(got, _explicit_rk(q, 0.2, np.asarray(t.a), np.asarray(t.b), rhs))
+
+
+def test_ark2_stable_on_stiff_linear_problem():
+    t = imexcore.ark2_tableau()
+    prob = ScalarProblem(-1000.0)
+    q = np.array([1.0])
+    for _ in range(50):
+        q = imexcore.ark_imex_step(q, 1.0, t, prob, lambda x: prob.linear(x))
+        assert np.all(np.isfinite(q)) and abs(q[0]) <= 1.0
+    assert abs(q[0]) < 1e-3
+
+
+def test_ark2_second_order_on_split_scalar():
+    t = imexcore.ark2_tableau()
+
+    def err(dt):
+        prob = ScalarProblem(-0.7)
+        q = np.array([1.0])
+        s = 0.0
+        while s < 1.0 - 1e-12:
+            q = imexcore.ark_imex_step(q, dt, t, prob, lambda x: -x)
+            s += dt
+        return abs(q[0] - np.exp(-1.0))
+    assert 1.8 < np.log2(err(0.1) / err(0.05)) < 2.2
+
+
+def test_imex_step_nan_detection():
+    with pytest.raises(FloatingPointError):
+        imexcore.ark_imex_step(np.array([1.0]), 0.1, imexcore.ark2_tableau(), ScalarProblem(0.0),
+                               lambda q: np.full_like(q, np.inf))
+
+
+def test_box_boundary_projectors_match_reference_semantics():
+    """euler.boundary_projectors (euler.py:218-258) on the slab: x faces, the
+    dummy y layer and the bottom/top lose their normal components; a corner
+    node loses all of them; interior nodes are not listed."""
+    mesh = specgrid.build_box_mesh(3, 2, 1000.0, 500.0, 2)
+    bidx, bproj = euler.boundary_projectors(mesh)
+    assert bproj.shape == (bidx.size, 3, 3)
+    d = np.diagonal(bproj, axis1=1, axis2=2)
+    assert np.all(d[:, 1] == 0.0)            # the slab's y faces bound every node
+    assert bidx.size == mesh.n_nodes          # so every node is a boundary node
+    m3 = specgrid.build_box_mesh_3d(2, 2, 2, 1.0, 1.0, 1.0, 2)
+    bidx3, bproj3 = euler.boundary_projectors(m3)
+    nel, nt, ns, nr = m3.nshape
+    interior = (np.arange(m3.n_nodes).reshape(m3.nshape)[0, 1, 1, 1])
+    assert interior not in set(bidx3.tolist())
