@@ -186,6 +186,25 @@ def cpu_threads():
     return os.cpu_count() or 1
 
 
+def cpu_model():
+    """lscpu model name of the host."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -200,10 +219,13 @@ def run_reference(args):
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": cfg["desc"], "sample": r["sample"],
                       "parallelism": "single host process (numpy)"},
-           "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": cpu_threads(),
-                            "kind": "port", "sample": r["sample"],
-                            "note": "oracle/hevi_oracle.py (numpy restatement of dycore); "
-                                    "OpenBLAS threads allowed, the 5x5 dgemms do not thread"},
+           "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": 1,
+                            "kind": "port", "sample": r["sample"], "cpu_model": cpu_model(),
+                            "host_threads_allowed": cpu_threads(),
+                            "note": "oracle/hevi_oracle.py (numpy restatement of dycore): a "
+                                    "single-threaded numpy program; OpenBLAS may use every host "
+                                    "thread but the 5x5 dgemms do not thread (SURVEY 6), so the "
+                                    "work runs on one core"},
            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -240,7 +262,11 @@ def run_gpu(args):
 
     if world == 1:
         plan = disc.plan_for(ref, sn)
-        plan.factor(lam)
+        torch.cuda.synchronize()
+        tf = time.perf_counter()
+        plan.factor(lam)      # columnsolve.get_factors: probe + banded LU (once per lam)
+        torch.cuda.synchronize()
+        factor_ms = 1e3 * (time.perf_counter() - tf)
         Q = plan.zeros()
         Q[..., :mesh.X].copy_(q0)
         work = plan.workspace()
@@ -250,7 +276,11 @@ def run_gpu(args):
     else:
         from paper_1702_04316_b200.distributed import DistributedStepper, grid_for
         px, py = grid_for(world)
-        ds = DistributedStepper(mesh, ref, disc, dt, px, py, rank, set_name=sn)
+        torch.cuda.synchronize()
+        tf = time.perf_counter()
+        ds = DistributedStepper(mesh, ref, disc, dt, px, py, rank, set_name=sn)   # factors in __init__
+        torch.cuda.synchronize()
+        factor_ms = 1e3 * (time.perf_counter() - tf)
         ds.load_global(q0)
         plan, Q, work = ds.plan, ds.Q, ds.work
 
@@ -408,7 +438,8 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not rk:
         r = reference_sample(args.cpu_steps, 1, budget_s=args.cpu_budget, cfg_name=args.config)
         cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": r["sample"], "ms_per_step": r["ms_per_step"]}
+               "sample": r["sample"], "ms_per_step": r["ms_per_step"], "cpu_model": cpu_model(),
+               "note": "single-threaded numpy oracle port of dycore (the reference path)"}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -427,6 +458,11 @@ def run_gpu(args):
                "storage_dof_per_s": 5 * mesh.n_nodes / (ms_step * 1e-3),
                "roofline": roof, "step_roofline": step_roof, "kernels": kern,
                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+               "setup": {"factor_ms": round(factor_ms, 3),
+                         "what": "columnsolve.get_factors on the device (k_lamtab + k_probe + "
+                                 "k_lu_dense: probe of lhs_schur, banded LU), once per lam; "
+                                 "outside the timed steps, as the reference builds it in its "
+                                 "first step (columnsolve.py:184-188)"},
                # fused HEVI step: 3 explicit stages (explicit_col: main + domain-end
                # kernel each) + 2 column solves [+ the P' plane of Q when not chained]
                # (set2c and RK35: 5 launches); plus, at N > 1, rank 0's halo kernels
@@ -514,10 +550,31 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)
+
+
+def self_launch(args) -> int:
+    """``python bench.py --gpus N`` without torchrun: launch N ranks (one
+    process per GPU) the way the driver does, and pass rank 0's line through."""
+    import socket
+    if args.impl != "reference":
+        import torch
+        if torch.cuda.device_count() < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but "
+                              f"{torch.cuda.device_count()} CUDA device(s) visible"}), flush=True)
+            return 1
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

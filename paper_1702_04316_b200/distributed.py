@@ -138,9 +138,12 @@ class HaloExchange:
         self.launches = 0   # halo pack/unpack kernels launched so far
 
     def _buf(self, key, shape, like):
+        """Reused buffer per (direction, phase, peer, shape): the stage state
+        (5 fields) and the P' plane (1 field) alternate without reallocating."""
         import torch
+        key = key + (tuple(shape),)
         b = self._bufs.get(key)
-        if b is None or tuple(b.shape) != tuple(shape):
+        if b is None:
             b = torch.empty(shape, dtype=like.dtype, device=like.device)
             self._bufs[key] = b
         return b
@@ -257,19 +260,28 @@ class LocalExchange:
         self.mesh, self.px, self.py = mesh, px, py
         self.plans = plans
 
-    def fill(self, rank, t_by_rank):
-        """Phase by phase, as HaloExchange: the sender's halo kernel packs the
-        region out of its window, the receiver's unpacks it into its own."""
-        me, phases = halo_plan(self.mesh, self.px, self.py, rank)
+    def fill(self, rank, t_by_rank, phases=(0, 1)):
+        """The given phases for one rank, as HaloExchange: the sender's halo
+        kernel packs the region out of its window, the receiver's unpacks it
+        into its own."""
+        me, plan = halo_plan(self.mesh, self.px, self.py, rank)
         w = me.window
-        for phase in phases:
-            for peer, sreg, rreg in phase:
+        for ip in phases:
+            for peer, sreg, rreg in plan[ip]:
                 if self.plans is not None and t_by_rank[rank].is_cuda:
                     buf = pack(self.plans[peer], t_by_rank[peer], rreg)
                     unpack(self.plans[rank], t_by_rank[rank], rreg, buf)
                 else:
                     pw = make_block(self.mesh, self.px, self.py, peer).window
                     _view(t_by_rank[rank], rreg, w).copy_(_view(t_by_rank[peer], rreg, pw))
+
+    def fill_all(self, t_by_rank):
+        """Phase 0 (x halos) on every rank, then phase 1 (y halos over the
+        whole x window, corners included) on every rank -- the order the real
+        exchange has, where each phase completes on all ranks before the next."""
+        for ip in (0, 1):
+            for r in range(len(t_by_rank)):
+                self.fill(r, t_by_rank, phases=(ip,))
 
 
 def run_local_partitioned(steppers, exchange: LocalExchange, nsteps=1):
@@ -285,6 +297,4 @@ def run_local_partitioned(steppers, exchange: LocalExchange, nsteps=1):
                 break
             lists = [it[1] for it in items]
             for j in range(len(lists[0])):
-                tensors = [lst[j] for lst in lists]
-                for r in range(len(steppers)):
-                    exchange.fill(r, tensors)
+                exchange.fill_all([lst[j] for lst in lists])

@@ -326,14 +326,23 @@ def run_simulation(cfg: RunConfig, quiet=False) -> RunResult:
     next_diag = cfg.diag_interval
     rhs = euler.make_rhs(ref, disc, set_name)
     q_prev = None                       # bdf2 history (device E-vector)
+    # the fused and RK35 steps overwrite Q in place and report failures only
+    # afterwards: keep the last good state so an aborted run writes it, as
+    # the reference does (cli.py:224-250 keeps q at the last good step)
+    Qgood = plan.empty() if (cfg.integrator == "rk35" or fused) else None
+    inplace = False
     t0 = time.perf_counter()
     exit_code, message = 0, ""
     try:
         while t < cfg.end_time - 1e-12:
             step_dt = min(dt, cfg.end_time - t)
+            if Qgood is not None:
+                Qgood.copy_(Q)
             if cfg.integrator == "rk35":
+                inplace = True
                 plan.rk35(step_dt, Q, work)
                 plan.check_flags()
+                inplace = False
             elif not fused and (cfg.integrator == "ark2" or q_prev is None or step_dt != dt):
                 # Krylov solves: the reference stage loop over the device operators
                 qn = plan.l2e(Q)
@@ -347,8 +356,10 @@ def run_simulation(cfg: RunConfig, quiet=False) -> RunResult:
                 lam = ark.diag * step_dt
                 plan.factor(lam)
                 problem.lam = lam
+                inplace = True
                 plan.step(step_dt, tarr, Q, work)
                 plan.check_flags()
+                inplace = False
                 problem.stats.solves += 2
             else:
                 qn = plan.l2e(Q)
@@ -364,6 +375,9 @@ def run_simulation(cfg: RunConfig, quiet=False) -> RunResult:
         exit_code, message = 3, str(exc)
     except FloatingPointError as exc:
         exit_code, message = 4, str(exc)
+    finally:
+        if inplace and Qgood is not None:
+            Q.copy_(Qgood)              # the failed in-place step never happened
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
 

@@ -53,3 +53,34 @@ def test_run_matches_reference_driver(name, tmp_path):
         s = max(np.abs(ref[:, list(cols)]).max(), fl)
         err = np.abs(snap[:, list(cols)] - ref[:, list(cols)]).max()
         assert err <= 1e-8 * s, (cols, err, s)
+
+
+@pytest.mark.parametrize("integrator", ["ark2", "rk35"])
+def test_aborted_run_writes_the_last_good_state(integrator, tmp_path, monkeypatch):
+    """A step that fails inside the fused (in-place) kernels leaves the
+    last good state in the snapshot, as the reference driver does
+    (cli.py:224-250): exit code 4, snapshot = the state after the good steps."""
+    from paper_1702_04316_b200.plan import HeviPlan
+    over = list(load("ark2")["overrides"])
+    over = [o for o in over if not o.startswith(("--integrator", "--end_time"))]
+    dt = float(load("ark2")["dt"])      # approximately this run's dt (the Courant rule)
+    name = "rk35" if integrator == "rk35" else "step"
+    orig = getattr(HeviPlan, name)
+    calls = {"n": 0}
+
+    def poisoned(self, *args, **kw):
+        calls["n"] += 1
+        if calls["n"] == 3:       # the third step starts from a corrupted state
+            args[-2 if name == "rk35" else 2][3].view(-1)[7] = float("nan")
+        return orig(self, *args, **kw)
+    monkeypatch.setattr(HeviPlan, name, poisoned)
+    bad = driver.run_simulation(driver.parse_config(None, over + [
+        f"--integrator={integrator}", f"--end_time={10 * dt}", f"--output_dir={tmp_path / 'bad'}"]), quiet=True)
+    monkeypatch.setattr(HeviPlan, name, orig)
+    good = driver.run_simulation(driver.parse_config(None, over + [
+        f"--integrator={integrator}", f"--end_time={2 * bad.dt!r}", f"--output_dir={tmp_path / 'good'}"]),
+        quiet=True)
+    assert good.exit_code == 0 and good.steps == 2
+    assert bad.exit_code == 4 and bad.steps == 2, (bad.exit_code, bad.steps, bad.message)
+    b, g = torch.as_tensor(bad.final_q), torch.as_tensor(good.final_q)
+    assert torch.equal(b, g), float((b - g).abs().max())
