@@ -87,8 +87,8 @@ def rk35_step(q, dt: float, rhs):
     ``euler.RHS`` the five stages run as fused device launches."""
     if isinstance(rhs, euler.RHS):
         plan = rhs.disc.plan_for(rhs.ref, rhs.set_name)
-        Q, back = plan.lattice_in(q)
-        work = plan.workspace()
+        Q, back = plan.lattice_in(q, reuse=True)
+        work = plan.cached_workspace()
         plan.rk35(dt, Q, work)
         plan.check_flags()
         return back(Q)
@@ -455,8 +455,8 @@ def ark_imex_step(q, dt: float, tableau: ButcherPair, problem, rhs):
         from .plan import tableau_array
         plan = problem.disc.plan_for(problem.ref, problem.set_name)
         problem.lam = tableau.diag * dt
-        Q, back = plan.lattice_in(q)
-        work = plan.workspace()
+        Q, back = plan.lattice_in(q, reuse=True)
+        work = plan.cached_workspace()
         plan.step(dt, tableau_array(tableau), Q, work)
         plan.check_flags()
         problem.stats.solves += 2

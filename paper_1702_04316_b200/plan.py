@@ -90,9 +90,17 @@ class HeviPlan:
         return torch.zeros((nf,) + self.shape[1:], dtype=torch.float64, device=self.device)
 
     def workspace(self):
-        """[Q1 | A | F | P] of the fused step."""
+        """[Q1 | A | F | P] of the fused step (a new zero-filled buffer)."""
         import torch
         return torch.zeros((4,) + self.shape, dtype=torch.float64, device=self.device)
+
+    def cached_workspace(self):
+        """The plan's persistent workspace for one-shot drop-in calls
+        (``imexcore.ark_imex_step``): allocated and zeroed once, then reused
+        -- every point a step reads is written earlier in the same step."""
+        if getattr(self, "_ws", None) is None:
+            self._ws = self.workspace()
+        return self._ws
 
     # -- conversions -----------------------------------------------------------
     def padded(self, L):
@@ -227,16 +235,34 @@ class HeviPlan:
         raise_for_flags(self.flags(reset=True))
 
     # -- reference-facing entry: E-vector in, E-vector out ------------------------
-    def lattice_in(self, q):
+    #: opt-in check that drop-in inputs are DSS-continuous (every copy of a
+    #: lattice point bitwise equal): the lattice keeps the first-occurrence
+    #: copy (columnsolve.unique_space rep), so a discontinuous E-vector would
+    #: silently give a different answer from the reference
+    check_continuity = False
+
+    def lattice_in(self, q, reuse=False):
         """E-vector (numpy / torch, host or device) -> (lattice tensor, back),
-        ``back`` returning the result in the caller's array type.  (Gathering
-        the unique copies straight from pinned host memory was measured no
-        faster than the DMA copy: PCIe sectors make the strided gather read
-        as many bytes, profiles/README.md.)"""
+        ``back`` returning the result in the caller's array type.  With
+        ``reuse`` the lattice is the plan's persistent buffer (overwritten by
+        the next call).  (Gathering the unique copies straight from pinned
+        host memory was measured no faster than the DMA copy: PCIe sectors
+        make the strided gather read as many bytes, profiles/README.md.)"""
         E, back0 = to_device(q)
         if E.shape != (5,) + tuple(self.mesh.nshape):
             raise ValueError("field/mesh shape mismatch")
-        return self.e2l(E), (lambda L: back0(self.l2e(L)))
+        if reuse:
+            if getattr(self, "_lat", None) is None:
+                self._lat = self.zeros()
+            L = self.e2l(E, out=self._lat)
+        else:
+            L = self.e2l(E)
+        if self.check_continuity:
+            back_e = self.l2e(L)
+            if not bool((back_e == E).all()):
+                raise ValueError("E-vector input is not DSS-continuous: coincident node copies "
+                                 "differ (the reference would average them; apply specgrid.apply_dss first)")
+        return L, (lambda L_: back0(self.l2e(L_)))
 
     # -- E-vector entry used by the drop-in operators ---------------------------
     def apply_evec(self, op, q, lam=None):

@@ -209,3 +209,23 @@ def test_host_and_device_inputs_give_bitwise_equal_steps(box3, integrator):
         outs.append(r.cpu().numpy() if isinstance(r, torch.Tensor) else r)
     assert isinstance(imexcore.rk35_step(qh, 0.05, rhs), torch.Tensor)
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_discontinuous_evector_rejected_when_checking():
+    """Opt-in DSS-continuity check of the drop-in entry (plan.lattice_in)."""
+    from paper_1702_04316_b200 import specgrid, euler, cases
+    mesh = specgrid.build_box_mesh_3d(3, 2, 2, 12_000.0, 8_000.0, 200.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    plan = disc.plan_for(ref)
+    q0 = cases.bubble_lattice(mesh, ref, 0.5, (6_000.0, 4_000.0, 100.0), (3000.0, 3000.0, 80.0))
+    E = plan.l2e(plan.padded(q0))
+    plan.check_continuity = True
+    try:
+        plan.lattice_in(E)                      # continuous: accepted
+        E2 = E.clone()
+        E2[0, 1, 0, 0, 0] += 1.0                # element 1's copy of a shared face node
+        with pytest.raises(ValueError):
+            plan.lattice_in(E2)
+    finally:
+        plan.check_continuity = False
