@@ -33,7 +33,8 @@
 
 #define EC_ZMAX 64
 #define EC_NMAX 4
-enum { C_RHO0 = 0, C_TH0, C_DRHO0, C_DTH0, C_CZ, C_IRHO0, C_G0, C_H0, C_PB, C_C0, C_IRT0, C_P0F, EC_NT };
+enum { C_RHO0 = 0, C_TH0, C_DRHO0, C_DTH0, C_CZ, C_IRHO0, C_G0, C_H0, C_PB, C_C0, C_IRT0, C_P0F,
+       C_TH0C, C_ITH0, C_F0C, EC_NT };   // set2c: Theta0 = rho0 theta0, 1/Theta0, F0 = gamma P0f / Theta0
 
 // per-level constants of the explicit_col kernels (N <= EC_NMAX, Z <= EC_ZMAX);
 // row(l) = l mod N (N on the top level), base(l) = l - row(l)

@@ -1187,6 +1187,7 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 
 #include "explicit_v2.cuh"
 #include "explicit_col.cuh"
+#include "explicit_colc.cuh"
 #include "explicit_c.cuh"
 #include "solve_v2.cuh"
 #include "imex3d.cuh"
@@ -1615,6 +1616,62 @@ int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     return HEVI_OK;
 }
 
+// set2c column sweep (explicit_colc.cuh): no P' plane (formed per level in the kernel)
+template <int N, int MODE>
+int launch_colc(const hevi_plan* pl, const EArgs& a0, cudaStream_t st) {
+    using T = ECC<N, MODE>;
+    const Geo& g = pl->g;
+    EArgs a = a0;
+    a.pp_out = nullptr;
+    static size_t attr[16] = {0};
+    auto kern = k_ecolc<N, MODE>;
+    int rc = set_smem_attr(kern, T::SMEM, attr);
+    if (rc) return rc;
+    CUtensorMap tq, tA, tF;
+    if ((rc = make_tmap(&tq, g, a.q, T::LXT, T::LY, 1))) return rc;
+    tA = tq;
+    tF = tq;
+    if (MODE == M_S2 && (rc = make_tmap(&tA, g, a.A, T::OX, T::OY, 1))) return rc;
+    if ((MODE == M_S2 || MODE == M_S3) && (rc = make_tmap(&tF, g, a.F, T::OX, T::OY, 1))) return rc;
+    const int nxc = (g.ex_e == g.nex) ? (g.ey_e - g.ey_b) * N + (g.ey_e == g.ney ? 1 : 0) : 0;
+    const int nyr = (g.ey_e == g.ney) ? (g.ex_e - g.ex_b) * N : 0;
+    const long long npt = (long long)(nxc + nyr) * g.Z;
+    const bool fork = npt > 0 && pl->side != nullptr;
+    if (fork) CK(cudaEventRecord(pl->ev_fork, st));
+    const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
+    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tA, tF);
+    CK(cudaGetLastError());
+    if (npt > 0) {
+        cudaStream_t es = fork ? pl->side : st;
+        if (fork) CK(cudaStreamWaitEvent(es, pl->ev_fork, 0));
+        k_ecolc_edge<N, MODE><<<(unsigned)((npt + 127) / 128), 128, 0, es>>>(a, pl->lt, nxc, nyr, g.ex_b * N,
+                                                                           g.ey_b * N);
+        CK(cudaGetLastError());
+        if (fork) {
+            CK(cudaEventRecord(pl->ev_join, es));
+            CK(cudaStreamWaitEvent(st, pl->ev_join, 0));
+        }
+    }
+    return HEVI_OK;
+}
+
+bool colc_applies(const hevi_plan* pl, int mode) {
+    const Geo& g = pl->g;
+    return pl->use_col && pl->use_tma && pl->lt_ok && pl->eqset == 1 && pl->N == 4 && pl->Ny == 4 &&
+           !g.slab && (g.x0 % 2) == 0 && (g.px % 2) == 0 &&
+           (mode == M_S1 || mode == M_S2 || mode == M_S3 || mode == M_R);
+}
+
+int run_colc(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
+    switch (mode) {
+        case M_R: return launch_colc<4, M_R>(pl, a, st);
+        case M_S1: return launch_colc<4, M_S1>(pl, a, st);
+        case M_S2: return launch_colc<4, M_S2>(pl, a, st);
+        case M_S3: return launch_colc<4, M_S3>(pl, a, st);
+    }
+    return fail("bad mode");
+}
+
 int run_col(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
     switch (mode) {
         case M_R: return launch_col<4, M_R>(pl, a, st);
@@ -1626,6 +1683,7 @@ int run_col(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
 }
 
 int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
+    if (colc_applies(pl, mode)) return run_colc(pl, mode, a, st);
     if (pl->eqset == 1) {
         switch (mode) {
             case M_R: return dispatch_c<M_R>(pl, a, st);
@@ -1986,6 +2044,9 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
             t.v[C_C0][k] = rd->Pb[k] - rd->P0f[k];
             t.v[C_IRT0][k] = 1.0 / (rd->rho0[k] * rd->theta0[k]);
             t.v[C_P0F][k] = rd->P0f[k];
+            t.v[C_TH0C][k] = rd->Theta0[k];
+            t.v[C_ITH0][k] = 1.0 / rd->Theta0[k];
+            t.v[C_F0C][k] = rd->F0c[k];
         }
         memcpy(t.dx, rd->Dx, sizeof(double) * nd);
         memcpy(t.dy, rd->Dy, sizeof(double) * ndy);
