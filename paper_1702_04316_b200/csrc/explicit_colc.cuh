@@ -43,15 +43,26 @@ struct ECC {
     static constexpr uint32_t AF_BYTES = (uint32_t)(sizeof(double) * AFB);
 };
 
-// P' of set2c about the background: P = P0 (R Theta / P0)^gamma, delta = Theta'/Theta0
-__device__ __forceinline__ double ecc_pprime(const EArgs& a, const LvlTab& lt, int gz, double rho, double Th) {
-    const double delta = Th * lt.v[C_ITH0][gz];
-    if (HEVI_PP_SHORT && fabs(delta) <= 0x1p-10) {
-        double s = a.bc[5];
+// P' of set2c about the background: P = P0 (R Theta / P0)^gamma, delta =
+// Theta'/Theta0; the level's constants and the short series' coefficients
+// are hoisted (PPc), the rare wide branch is out of line with scalar args
+struct PPc {
+    double ith0, pb, c0;
+    double b[6];
+};
+
+__device__ __forceinline__ PPc ecc_ppc(const EArgs& a, const LvlTab& lt, int gz) {
+    PPc c;
+    c.ith0 = lt.v[C_ITH0][gz];
+    c.pb = lt.v[C_PB][gz];
+    c.c0 = lt.v[C_C0][gz];
 #pragma unroll
-        for (int k = 4; k >= 0; --k) s = fma(s, delta, a.bc[k]);
-        return fma(lt.v[C_PB][gz], s * delta, lt.v[C_C0][gz]);
-    }
+    for (int k = 0; k < 6; ++k) c.b[k] = a.bc[k];
+    return c;
+}
+
+__device__ __noinline__ double ecc_pprime_wide(const EArgs& a, const LvlTab& lt, int gz, double delta,
+                                               double rho, double Th) {
     if (fabs(delta) <= 0.125) {
         double s = a.bc[14];
 #pragma unroll
@@ -60,6 +71,22 @@ __device__ __forceinline__ double ecc_pprime(const EArgs& a, const LvlTab& lt, i
     }
     const double theta = (lt.v[C_TH0C][gz] + Th) / rho;
     return a.ph.P0 * pow(rho * a.ph.R * theta / a.ph.P0, a.ph.gamma) - lt.v[C_P0F][gz];
+}
+
+__device__ __forceinline__ double ecc_pprime(const EArgs& a, const LvlTab& lt, int gz, const PPc& c, double rho,
+                                             double Th) {
+    const double delta = Th * c.ith0;
+    if (HEVI_PP_SHORT && fabs(delta) <= 0x1p-10) {
+        double s = c.b[5];
+#pragma unroll
+        for (int k = 4; k >= 0; --k) s = fma(s, delta, c.b[k]);
+        return fma(c.pb, s * delta, c.c0);
+    }
+    return ecc_pprime_wide(a, lt, gz, delta, rho, Th);
+}
+
+__device__ __forceinline__ double ecc_pprime(const EArgs& a, const LvlTab& lt, int gz, double rho, double Th) {
+    return ecc_pprime(a, lt, gz, ecc_ppc(a, lt, gz), rho, Th);
 }
 
 // R, L_V of set2c at a point from its 16 derivative values (euler.py:481-487, 350-361)
@@ -181,13 +208,15 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
         const double* slot = ring + (l % S) * SS;
         double* pb = PB + (l & 1) * T::PBS;
         const double rho0 = lt.v[C_RHO0][l], Th0 = lt.v[C_TH0C][l];
+        const PPc ppc = ecc_ppc(a, lt, l);
+#pragma unroll 1
         for (int i = tid; i < LY * LXT; i += BLK) {
             const double r = slot[i], U = slot[PL + i], V = slot[2 * PL + i], W = slot[3 * PL + i],
                          Th = slot[4 * PL + i];
             const double rho = rho0 + r;
             const double irho = 1.0 / rho;
             const double theta = (Th0 + Th) * irho;
-            const double pp = ecc_pprime(a, lt, l, rho, Th);
+            const double pp = ecc_pprime(a, lt, l, ppc, rho, Th);
             pb[0 * PL + i] = (U * U) * irho + pp;
             pb[1 * PL + i] = (U * V) * irho;
             pb[2 * PL + i] = (U * W) * irho;
@@ -203,6 +232,7 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
         const double* pb = PB + (l & 1) * T::PBS;
         double* xf = XFb + buf * T::NXF;
         double* yf = YFb + buf * T::NYF;
+#pragma unroll 1
         for (int i = tid; i < T::NXF + T::NYF; i += BLK) {
             if (i < T::NXF) {
                 const int q = i / (OY * TX), rem = i % (OY * TX);
