@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
         Dxr[m] = cxv * sD[rx * (N + 1) + m];
         Dyr[m] = cyv * sD[T::DN + ry * (N + 1) + m];
     }
-    const double fxs = (rx == 0) ? cxv : 0.0, fys = (ry == 0) ? cyv : 0.0;
+    // element-face weights; the domain's low walls (gx = 0, gy = 0) have no lower element
+    const double fxs = (rx == 0 && gx > 0) ? cxv : 0.0, fys = (ry == 0 && gy > 0) ? cyv : 0.0;
     const bool bx = (gx == 0), by = (gy == 0);
     const int lx = ox + N, ly = oy + N;
     const int xo = ly * LXT + (lx - rx);

@@ -1275,6 +1275,7 @@ struct hevi_plan {
     // it runs in the main kernel's last, partial wave (capturable in graphs)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    double* ppscratch = nullptr;   // hevi_rhs on the column sweep: P'(q) of the caller's state
     LvlTab lt;               // per-level constants of the explicit_col kernels
 };
 
@@ -2088,6 +2089,7 @@ int hevi_plan_destroy(hevi_plan* pl) {
         cudaFree(kv.second.piv);
         cudaFree(kv.second.d_info);
     }
+    if (pl->ppscratch) cudaFree(pl->ppscratch);
     if (pl->side) cudaStreamDestroy(pl->side);
     if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
     if (pl->ev_join) cudaEventDestroy(pl->ev_join);
@@ -2176,12 +2178,30 @@ int hevi_column_matrix(hevi_plan* pl, double lam, double* A_host, double* LU_hos
     return HEVI_OK;
 }
 
+// the fused step chains P' of the stage-0 input through stage 2 of the
+// previous step (explicit_col M_S3 writes P'(Q^{n+1}) into work's Q1 field 0)
+static bool pp_chainable(const hevi_plan* pl) {
+    const Geo& g = pl->g;
+    return pl->use_col && pl->use_v2 && pl->use_tma && pl->lt_ok && pl->eqset == 0 && pl->N == 4 &&
+           pl->Ny == 4 && !g.slab && (g.x0 % 2) == 0 && (g.px % 2) == 0;
+}
+
 int hevi_rhs(hevi_plan* pl, const double* q, double* R, void* stream) {
     if (!pl || !q || !R) return fail("null argument");
     EArgs a = base_eargs(pl);
     a.q = q;
     a.out = R;
     a.stage = 0;
+    if (pl->eqset == 0 && pp_chainable(pl)) {
+        // the production column sweep reads P'(q) as a plane: form it first
+        if (!pl->ppscratch) CK(cudaMalloc(&pl->ppscratch, sizeof(double) * pl->g.fs));
+        BC16 bcv;
+        memcpy(bcv.v, pl->bc, sizeof(bcv.v));
+        const dim3 grid((pl->g.lX + 255) / 256, pl->g.lY, pl->g.Z);
+        k_pp_plane<<<grid, 256, 0, (cudaStream_t)stream>>>(pl->g, pl->lv, pl->ph, q, pl->ppscratch, bcv);
+        CK(cudaGetLastError());
+        a.pp_in = pl->ppscratch;
+    }
     return run_e(pl, M_R, a, (cudaStream_t)stream);
 }
 
@@ -2203,14 +2223,6 @@ int hevi_solve(hevi_plan* pl, double lam, const double* qe, double* q, void* str
     a.out = q;
     a.src_uv = qe;
     return run_s(pl, a, (cudaStream_t)stream);
-}
-
-// the fused step chains P' of the stage-0 input through stage 2 of the
-// previous step (explicit_col M_S3 writes P'(Q^{n+1}) into work's Q1 field 0)
-static bool pp_chainable(const hevi_plan* pl) {
-    const Geo& g = pl->g;
-    return pl->use_col && pl->use_v2 && pl->use_tma && pl->lt_ok && pl->eqset == 0 && pl->N == 4 &&
-           pl->Ny == 4 && !g.slab && (g.x0 % 2) == 0 && (g.px % 2) == 0;
 }
 
 int hevi_pp_refresh(hevi_plan* pl, const double* Q, double* work, void* stream) {

@@ -67,33 +67,35 @@ def make_block(mesh, px: int, py: int, rank: int) -> Block:
 
 
 def halo_plan(mesh, px, py, rank):
-    """List of transfers (peer, send_region, recv_region) for one rank.
+    """List of transfers (peer, send_region, recv_region) for one rank, as
+    phases.  Regions are (xlo, xhi, ylo, yhi) in GLOBAL lattice indices.
 
-    Regions are (xlo, xhi, ylo, yhi) in GLOBAL lattice indices.  Phase 1
-    exchanges x halos over the owned y rows, phase 2 exchanges y halos over
-    the whole x window (so corner halos are filled too)."""
+    One phase: the x halos over the owned rows and the y halos over the owned
+    columns.  The explicit kernels never read a corner halo point (their x-lines
+    and x-face partials lie on owned rows, their y-lines and y-face partials on
+    owned columns), so no second phase is needed to fill corners; the
+    partitioned-equals-single-GPU tests would catch any corner read (stale
+    corners are never refreshed)."""
     me = make_block(mesh, px, py, rank)
     N, Ny = mesh.N, mesh.Ny
-    w = me.window
     oy0, oy1 = me.ey[0] * Ny, me.ey[1] * Ny + (1 if me.ey[1] == mesh.ny else 0)
     ox0, ox1 = me.ex[0] * N, me.ex[1] * N + (1 if me.ex[1] == mesh.nx else 0)
-    phases = [[], []]
+    phase = []
     if me.ix > 0:       # left neighbour owns [ex0*N - N, ex0*N); I own ex0*N (its high halo)
         L = rank - 1
-        phases[0].append((L, (ox0, ox0 + 1, oy0, oy1), (ox0 - N, ox0, oy0, oy1)))
+        phase.append((L, (ox0, ox0 + 1, oy0, oy1), (ox0 - N, ox0, oy0, oy1)))
     if me.ix < px - 1:  # right neighbour owns ex1*N (my high halo); it needs my last N columns
         R = rank + 1
         x1 = me.ex[1] * N
-        phases[0].append((R, (x1 - N, x1, oy0, oy1), (x1, x1 + 1, oy0, oy1)))
-    xw0, xw1 = w["x0"], w["x0"] + w["lX"]
+        phase.append((R, (x1 - N, x1, oy0, oy1), (x1, x1 + 1, oy0, oy1)))
     if me.iy > 0:
         D = rank - px
-        phases[1].append((D, (xw0, xw1, oy0, oy0 + 1), (xw0, xw1, oy0 - Ny, oy0)))
+        phase.append((D, (ox0, ox1, oy0, oy0 + 1), (ox0, ox1, oy0 - Ny, oy0)))
     if me.iy < py - 1:
         U = rank + px
         y1 = me.ey[1] * Ny
-        phases[1].append((U, (xw0, xw1, y1 - Ny, y1), (xw0, xw1, y1, y1 + 1)))
-    return me, phases
+        phase.append((U, (ox0, ox1, y1 - Ny, y1), (ox0, ox1, y1, y1 + 1)))
+    return me, [phase]
 
 
 def _view(t, region, w):
@@ -260,7 +262,7 @@ class LocalExchange:
         self.mesh, self.px, self.py = mesh, px, py
         self.plans = plans
 
-    def fill(self, rank, t_by_rank, phases=(0, 1)):
+    def fill(self, rank, t_by_rank, phases=(0,)):
         """The given phases for one rank, as HaloExchange: the sender's halo
         kernel packs the region out of its window, the receiver's unpacks it
         into its own."""
@@ -276,10 +278,10 @@ class LocalExchange:
                     _view(t_by_rank[rank], rreg, w).copy_(_view(t_by_rank[peer], rreg, pw))
 
     def fill_all(self, t_by_rank):
-        """Phase 0 (x halos) on every rank, then phase 1 (y halos over the
-        whole x window, corners included) on every rank -- the order the real
-        exchange has, where each phase completes on all ranks before the next."""
-        for ip in (0, 1):
+        """Every phase on every rank before the next phase, the order the real
+        exchange has (one phase: x halos on owned rows, y halos on owned columns)."""
+        nph = len(halo_plan(self.mesh, self.px, self.py, 0)[1])
+        for ip in range(nph):
             for r in range(len(t_by_rank)):
                 self.fill(r, t_by_rank, phases=(ip,))
 
