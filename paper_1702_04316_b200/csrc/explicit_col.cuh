@@ -47,6 +47,14 @@ struct LvlTab {
     double cg[EC_ZMAX][5], ch[EC_ZMAX][5];   // Dz[N][m] * G0 / H0 [l + m]: row-N carry of P_lin, layer base l
 };
 
+// TMA bulk tensor store of one staged box (shared::cta -> global)
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+        "r"((unsigned)__cvta_generic_to_shared(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
 template <int N, int MODE>
 struct EC {
     static constexpr int TX = 4, TY = 4;                      // elements per tile
@@ -62,11 +70,16 @@ struct EC {
     static constexpr int SAF = NAF ? 2 : 0;                   // A/F level slots
     static constexpr int SAFM = NAF ? SAF : 1;                // (modulus when SAF is 0)
     static constexpr int AFB = 5 * OX * OY;                   // one array's box
-    static constexpr int S = NAF ? 6 : 8;                     // ring slots
+    // stage 0's A and F outputs (10 planes) leave by TMA bulk tensor stores
+    // from a double-buffered staging area: no per-store address arithmetic.
+    // (Staging every output of every stage measured slower: 3.48 vs 3.27 ms.)
+    static constexpr int NOUT = (MODE == M_S1) ? 10 : 0;
+    static constexpr int S = NAF ? 6 : (NOUT ? 7 : 8);        // ring slots
     static constexpr int NXF = 6 * OY * TX, NYF = 6 * TY * OX;   // face partials per level
     static constexpr int DN = (N + 1) * (N + 1);
     static constexpr size_t SMEM =
-        sizeof(double) * ((size_t)S * SS + (size_t)SAF * NAF * AFB + 2 * (NXF + NYF) + 2 * DN + OX + OY) +
+        sizeof(double) * ((size_t)S * SS + (size_t)SAF * NAF * AFB + 2 * (size_t)NOUT * OX * OY +
+                          2 * (NXF + NYF) + 2 * DN + OX + OY) +
         sizeof(uint64_t) * (S + SAF) + 128;
     static constexpr uint32_t LVL_BYTES = (uint32_t)(sizeof(double) * 5 * PL);
     static constexpr uint32_t PP_BYTES = (uint32_t)(sizeof(double) * PL);
@@ -200,7 +213,9 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     k_ecol(const EArgs a, const __grid_constant__ LvlTab lt, const __grid_constant__ CUtensorMap tmq,
            const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmA,
-           const __grid_constant__ CUtensorMap tmF) {
+           const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmO0,
+           const __grid_constant__ CUtensorMap tmO1, const __grid_constant__ CUtensorMap tmO2,
+           const __grid_constant__ CUtensorMap tmO3) {
     using T = EC<N, MODE>;
     constexpr int PL = T::PL, LXT = T::LXT, SS = T::SS, S = T::S, BLK = T::BLK;
     constexpr int OX = T::OX, OY = T::OY, TX = T::TX, TY = T::TY;
@@ -211,7 +226,8 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     double* ring = reinterpret_cast<double*>(
         smraw + ((128u - ((unsigned)__cvta_generic_to_shared(smraw) & 127u)) & 127u));
     double* sAF = ring + S * SS;          // [SAF][NAF][5][OY][OX]: A (M_S2) | F
-    double* XFb = sAF + T::SAF * T::NAF * T::AFB;   // [2][NXF]  XF[f][oy][j]
+    double* sOut = sAF + T::SAF * T::NAF * T::AFB;  // [2][NOUT][OY][OX] staged outputs (TMA store sources)
+    double* XFb = sOut + 2 * T::NOUT * OX * OY;     // [2][NXF]  XF[f][oy][j]
     double* YFb = XFb + 2 * T::NXF;       // [2][NYF]  YF[f][j][ox]
     double* sD = YFb + 2 * T::NYF;        // Dx | Dy
     double* sC = sD + 2 * T::DN;          // cx of the tile's columns | cy of its rows
@@ -439,10 +455,42 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
             double Rv[5], Lv[5];
             ec_finish<MODE>(p, c, rho0, lt.v[C_DRHO0][l], lt.v[C_DTH0][l], lt.v[C_IRHO0][l], gr, bx, by,
                             (l == 0) || top, Rv, Lv);
-            ec_epilogue<MODE>(a, lt, o, l, p, Rv, Lv, Ai, Fi, bx, by);
+            if (T::NOUT) {
+                // imexcore.py:398-403, 409-411: P, Quv by plain stores, A and F staged
+                const double dt = a.dt;
+                const double qv[5] = {p.r, p.u, p.v, p.w, p.th};
+                double* so = sOut + (l & 1) * (T::NOUT * OX * OY) + tid;
+                double pr[5];
+#pragma unroll
+                for (int f = 0; f < 5; ++f) {
+                    pr[f] = qv[f] + dt * (a.a_p * (Rv[f] - Lv[f]) + a.at_p * Lv[f]);
+                    so[f * OX * OY] = qv[f] + dt * (a.a_a * (Rv[f] - Lv[f]) + a.at_a * Lv[f]);
+                    so[(5 + f) * OX * OY] = qv[f] + a.cb * Rv[f];
+                }
+                const long long fs = g.fs;
+                a.P[o] = pr[0];
+                a.P[o + 3 * fs] = pr[3];
+                a.P[o + 4 * fs] = pr[4];
+                a.Quv[o + fs] = bx ? 0.0 : pr[1];
+                a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+            } else {
+                ec_epilogue<MODE>(a, lt, o, l, p, Rv, Lv, Ai, Fi, bx, by);
+            }
         }
         if (l + 1 < Z) faces(l + 1, (l + 1) & 1);
+        if (T::NOUT) {
+            // staged outputs visible to the async proxy; the store that read
+            // the other staging buffer (level l-1) has finished reading it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncthreads();
+        if (T::NOUT && tid == 0) {
+            const double* so = sOut + (l & 1) * (T::NOUT * OX * OY);
+            tma_store_4d(&tmO0, so, ax0, ay0, l, 0);                  // A
+            tma_store_4d(&tmO1, so + 5 * OX * OY, ax0, ay0, l, 0);    // F
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
         // refills of the slots level l used; the issuing warp rotates so the
         // issue latency does not always fall on the same warp
         if (tid == 32 * (l % (BLK / 32)) && (l + S < Z || (T::NAF && l + T::SAF < Z))) {
@@ -453,6 +501,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
         }
         if (!top) k = (k + 1 == N) ? 0 : k + 1;
     }
+    if (T::NOUT && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // the domain-end planes x = X-1 / y = Y-1 inside the rank's ownership: one

@@ -1578,6 +1578,23 @@ bool col_applies(const hevi_plan* pl, int mode, const EArgs& a) {
            (mode == M_S1 || mode == M_S2 || mode == M_S3 || mode == M_R);
 }
 
+// 4D map over a 5-field lattice array whose box covers nf consecutive fields
+// (the field coordinate of a copy selects the first one)
+int make_tmap_fields(CUtensorMap* m, const Geo& g, const double* base, int bx, int by, int nf) {
+    PFN_encodeTiled_t enc = encode_fn();
+    if (!enc) return fail("cuTensorMapEncodeTiled unavailable");
+    if (((uintptr_t)base & 15) || (g.px & 1)) return fail("lattice arrays must be 16-byte aligned with even pitch");
+    cuuint64_t dims[4] = {(cuuint64_t)g.lX, (cuuint64_t)g.lY, (cuuint64_t)g.Z, 5};
+    cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.lY * g.px * 8, (cuuint64_t)g.fs * 8};
+    cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, 1, (cuuint32_t)nf};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled failed");
+    return HEVI_OK;
+}
+
 template <int N, int MODE>
 int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     using T = EC<N, MODE>;
@@ -1593,14 +1610,24 @@ int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     tF = tq;
     if (MODE == M_S2 && (rc = make_tmap(&tA, g, a.A, T::OX, T::OY, 1))) return rc;
     if ((MODE == M_S2 || MODE == M_S3) && (rc = make_tmap(&tF, g, a.F, T::OX, T::OY, 1))) return rc;
+    // TMA store destinations of stage 0's staged A and F (see EC::NOUT)
+    CUtensorMap o0 = tq, o1 = tq, o2 = tq, o3 = tq;
+    if (MODE == M_S1) {
+        if ((rc = make_tmap_fields(&o0, g, a.A, T::OX, T::OY, 5))) return rc;
+        if ((rc = make_tmap_fields(&o1, g, a.F, T::OX, T::OY, 5))) return rc;
+    }
     // domain-end planes owned by this rank
     const int nxc = (g.ex_e == g.nex) ? (g.ey_e - g.ey_b) * N + (g.ey_e == g.ney ? 1 : 0) : 0;
     const int nyr = (g.ey_e == g.ney) ? (g.ex_e - g.ex_b) * N : 0;
     const long long npt = (long long)(nxc + nyr) * g.Z;
-    const bool fork = npt > 0 && pl->side != nullptr;
+    // a partial tile at a domain end stores whole staging boxes, which cover
+    // the domain-end plane: the edge kernel must then run after the sweep
+    const bool partial_end = ((g.ex_e == g.nex) && (g.ex_e - g.ex_b) % T::TX != 0) ||
+                             ((g.ey_e == g.ney) && (g.ey_e - g.ey_b) % T::TY != 0);
+    const bool fork = npt > 0 && pl->side != nullptr && !(T::NOUT && partial_end);
     if (fork) CK(cudaEventRecord(pl->ev_fork, st));
     const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
-    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF);
+    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF, o0, o1, o2, o3);
     CK(cudaGetLastError());
     if (npt > 0) {
         // launched after the sweep: its blocks are dispatched as the sweep's last CTAs retire
