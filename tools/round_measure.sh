@@ -19,10 +19,15 @@ ncu --set full --import-source on --clock-control none -k regex:^k_ecol$ --launc
 ncu --set full --import-source on --clock-control none -k regex:^k_solve2$ --launch-skip 6 \
     --launch-count 2 -f -o gpurun_out/${tag}_s python bench.py --steps 1 --warmup 3 --no-e2e \
     --no-cpu-baseline > gpurun_out/${tag}_ncu_s.log 2>&1
-for r in e s; do
+# set2c (flux form): bench line and one explicit stage-1 launch
+python bench.py --set set2c --steps 20 --no-e2e > gpurun_out/${tag}_bench_set2c.json 2>&1
+ncu --set full --import-source on --clock-control none -k regex:^k_ecolc$ --launch-skip 10 \
+    --launch-count 1 -f -o gpurun_out/${tag}_c python bench.py --set set2c --steps 1 --warmup 3 \
+    --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu_c.log 2>&1
+for r in e s c; do
   ncu -i gpurun_out/${tag}_$r.ncu-rep --page raw --csv > gpurun_out/${tag}_${r}_raw.csv 2>/dev/null
   ncu -i gpurun_out/${tag}_$r.ncu-rep --page source --csv --print-source=sass > gpurun_out/${tag}_${r}_src.csv 2>/dev/null
 done
 gzip -f gpurun_out/${tag}_*_src.csv
-rm -f gpurun_out/${tag}_e.ncu-rep gpurun_out/${tag}_s.ncu-rep
+rm -f gpurun_out/${tag}_[esc].ncu-rep
 tail -1 gpurun_out/${tag}_bench.json | cut -c1-400
