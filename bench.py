@@ -137,6 +137,27 @@ def dist_env():
     return world, rank, local
 
 
+def count_launches(fn):
+    """Kernel launches of one call of ``fn`` seen by the CUDA activity
+    profiler (untimed): (ours, total) where ``ours`` are the library's
+    kernels (k_* / k3_*), or None when the profiler is unavailable."""
+    import re
+    import torch
+    try:
+        from torch.profiler import profile, ProfilerActivity
+        from torch.autograd import DeviceType
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type == DeviceType.CUDA
+                 and not e.name.startswith(("Memcpy", "Memset"))]
+    except Exception:
+        return None
+    ours = [n for n in names if re.search(r"(^|::|\s)k3?_\w+", n)]
+    return len(ours), len(names)
+
+
 def ncu_traffic():
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu
     summary (profiles/), or None."""
@@ -297,7 +318,12 @@ def run_gpu(args):
     # algorithmic bytes: with the chained P' plane stage 0 reads it from the
     # previous stage 2 (which writes it) instead of a separate k_pp_plane pass
     kb = dict(KERNEL_BYTES_PER_POINT)
-    if chain:
+    if args.set == "set2c":
+        # flux form: no P' planes (the explicit kernels form EOS per point)
+        kb = {"explicit_stage0": 8 * (5 + 15), "solve_stage0": 8 * (3 + 3),
+              "explicit_stage1": 8 * (15 + 10), "solve_stage1": 8 * (3 + 3),
+              "explicit_stage2": 8 * (10 + 5)}
+    elif chain:
         kb["explicit_stage0"] = 8 * (5 + 1 + 15)
         kb["explicit_stage2"] = 8 * (10 + 1 + 5 + 1)
     step_bytes = sum(kb.values())
@@ -408,15 +434,23 @@ def run_gpu(args):
         kb["rk35_step"] = 8 * 5 * 18
         ktimes = {"rk35_step": elapsed}
         names = ["rk35_step"]
-    if rk or args.set != "set2nc":
+    # launches per step: counted by the CUDA activity profiler on one extra
+    # (untimed) step; the static schedule count if the profiler is unavailable
+    counted = count_launches(one_step)
+    plan.check_flags()
+    if counted is not None:
+        launches_per_step = counted[0]
+        halo_launches = 0     # the halo kernels run inside one_step and are counted
+    elif rk:
         launches_per_step = 5
     else:
-        launches_per_step = 8 if chain else 6
+        launches_per_step = 8 if chain or args.set != "set2nc" else 9
     dom = max(names, key=lambda n: ktimes[n])
     traffic = None
     summ = ncu_traffic()
-    if summ and args.config in summ and dom in summ[args.config]:
-        traffic = summ[args.config][dom].get("dram_bytes_per_launch")
+    skey = args.config if args.set == "set2nc" else args.config + ":" + args.set
+    if summ and skey in summ and dom in summ[skey]:
+        traffic = summ[skey][dom].get("dram_bytes_per_launch")
     achieved = kern[dom]["alg_GBps"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -464,9 +498,13 @@ def run_gpu(args):
                                  "outside the timed steps, as the reference builds it in its "
                                  "first step (columnsolve.py:184-188)"},
                # fused HEVI step: 3 explicit stages (explicit_col: main + domain-end
-               # kernel each) + 2 column solves [+ the P' plane of Q when not chained]
-               # (set2c and RK35: 5 launches); plus, at N > 1, rank 0's halo kernels
-               "gpu_launches": launches_per_step * args.steps + halo_launches}
+               # kernel each) + 2 column solves [+ the P' plane of Q when not chained];
+               # at N > 1 plus the halo pack/unpack kernels
+               "gpu_launches": launches_per_step * args.steps + halo_launches,
+               "launches_per_step": {"ours": launches_per_step,
+                                     "all_kernels": counted[1] if counted else None,
+                                     "source": "torch.profiler CUDA activity, one untimed step"
+                                     if counted else "static schedule count"}}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -41,6 +41,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1241,6 +1242,7 @@ struct Factor {
     double* vtab = nullptr;    // 12*M
     double* LU2 = nullptr;     // M*(4N+1)
     double* rU = nullptr;      // M
+    double* rec = nullptr;     // M * RS: k_solve2's per-level records
     int* d_nb = nullptr;
     unsigned* d_bad = nullptr; // degenerate no-pivot diagonal seen
     int pivoted = 0;           // factor_with_fallback took the pivoted path
@@ -1810,6 +1812,7 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
     a.src_uv = a1.src_uv;
     a.pp_out = a1.pp_out;
     a.lv = pl->lv;
+    a.rec = f->rec;
     memcpy(a.bc, pl->bc, sizeof(a.bc));
     const int T = 128;
     if (f->pivoted) {   // columnsolve.factor_with_fallback: pivoted dense factor
@@ -1826,8 +1829,7 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
         CK(cudaGetLastError());
         return HEVI_OK;
     }
-    const size_t smem = sizeof(double) * ((size_t)V_NT * M + (size_t)M * (4 * N + 1) + M +
-                                          (N + 1) * (N + 1) + 6 * (size_t)M + (size_t)M * T);
+    const size_t smem = s2_smem_bytes<N>(M, T);
     if (smem > 225 * 1024) return fail("column too tall for the v2 column kernel");
     static size_t attr = 0;
     if (attr < smem) {
@@ -1838,7 +1840,7 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
     const int NYo = g.slab ? 1 : pl->N;
     const long long cntx = (long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0);
     const long long cnty = (long long)(g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
-    const int blocks = (int)((cntx * cnty + T - 1) / T);
+    const int nblk = (int)((cntx * cnty + T - 1) / T);
     if (pl->eqset == 1) {
         static size_t attrc = 0;
         if (attrc < smem) {
@@ -1846,10 +1848,15 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
                                     (int)smem));
             attrc = smem;
         }
-        k_solve2<N, true><<<blocks, T, smem, st>>>(a);
-    } else {
-        k_solve2<N, false><<<blocks, T, smem, st>>>(a);
     }
+    auto kern = pl->eqset == 1 ? k_solve2<N, true> : k_solve2<N, false>;
+    // persistent grid: every resident CTA slot once (the records load once per CTA)
+    int per_sm = 0, dev = 0, nsm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int blocks = std::max(1, std::min(nblk, per_sm * nsm));
+    kern<<<blocks, T, smem, st>>>(a);
     CK(cudaGetLastError());
     return HEVI_OK;
 }
@@ -1857,8 +1864,8 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
 int run_s2(const hevi_plan* pl, const Factor* f, const SArgs& a, cudaStream_t st, bool& done) {
     done = false;
     if (!pl->use_v2 || (f->nb > 2 * pl->N + 1 && !f->pivoted)) return HEVI_OK;
-    const size_t need = sizeof(double) * ((size_t)V_NT * pl->g.Z +
-                                          (size_t)pl->g.Z * (4 * pl->N + 1 + 1 + 6 + 128));
+    const size_t need = sizeof(double) * ((size_t)pl->g.Z * (4 * pl->N + 2 + (V_NT + 1) / 2 * 2 + 6 + 128) +
+                                          (size_t)(pl->N + 1) * (pl->N + 1));   // s2_smem_bytes
     if (need > 220 * 1024) return HEVI_OK;
     int rc = HEVI_OK;
     switch (pl->N) {
@@ -2110,6 +2117,7 @@ int hevi_plan_destroy(hevi_plan* pl) {
         cudaFree(kv.second.vtab);
         cudaFree(kv.second.LU2);
         cudaFree(kv.second.rU);
+        cudaFree(kv.second.rec);
         cudaFree(kv.second.d_nb);
         cudaFree(kv.second.d_bad);
         cudaFree(kv.second.LUP);
@@ -2171,6 +2179,12 @@ int hevi_factor(hevi_plan* pl, double lam, int* nb_out, void* stream) {
         CK(cudaGetLastError());
         k_lu_dense<<<1, 256, 0, st>>>(f.A, f.LU, f.LUb, M, f.d_nb, f.d_bad, pl->N, f.LU2, f.rU);
         CK(cudaGetLastError());
+        {
+            const int RS = 4 * pl->N + 2 + (V_NT + 1) / 2 * 2 + 6;
+            CK(cudaMalloc(&f.rec, sizeof(double) * M * RS));
+            k_s2rec<<<(M * RS + 255) / 256, 256, 0, st>>>(f.LU2, f.rU, f.vtab, pl->lv, M, pl->N, f.rec);
+            CK(cudaGetLastError());
+        }
         unsigned bad = 0;
         CK(cudaMemcpyAsync(&f.nb, f.d_nb, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(&bad, f.d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st));

@@ -54,16 +54,23 @@ def main():
         out[f"explicit_stage{i}"] = d
     for i, d in enumerate(s):
         out[f"solve_stage{i}"] = d
-    summ = {cfg: out, "source": f"tools/round_measure.sh {tag}: ncu --set full --clock-control none, "
-                                "first timed step of bench.py --steps 1 --warmup 3"}
+    summ = {cfg: out}
+    cpath = os.path.join(ROOT, "gpurun_out", f"{tag}_c_raw.csv")
+    if os.path.exists(cpath):   # set2c: explicit stage 1 (k_ecolc M_S2)
+        summ[cfg + ":set2c"] = {"explicit_stage1": list(rows_of(cpath))[0]}
+    summ["source"] = (f"tools/round_measure.sh {tag}: ncu --set full --clock-control none, "
+                      "first timed step of bench.py --steps 1 --warmup 3 [--set set2c]")
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
         json.dump(summ, f, indent=1)
-    for k, d in out.items():
+    rows = list(out.items()) + [("set2c " + k, d) for k, d in summ.get(cfg + ":set2c", {}).items()]
+    for k, d in rows:
         print(f"{k:16s} {d['time_s'] * 1e3:7.3f} ms  dram {d['dram_bytes_per_launch'] / 1e9:6.3f} GB "
               f"({d['dram_GBps']:7.1f} GB/s)  issue {float(d[KEYS[3]]):5.1f}%  warps "
               f"{float(d[KEYS[5]]):5.1f}%  regs {d[KEYS[6]]}  inst {float(d[KEYS[4]]):.3e}  "
               f"fp64 {float(d[KEYS[7]]):5.1f}%  bank-conflict wavefronts "
               f"{float(d[KEYS[8]]) / max(float(d[KEYS[9]]), 1):.3f}")
+        print("    stalls/issue: long_sb %.2f barrier %.2f short_sb %.2f wait %.2f mio %.2f"
+              % tuple(float(d.get(k, "nan")) for k in KEYS[11:16]))
 
 
 if __name__ == "__main__":
