@@ -146,6 +146,15 @@ __device__ __forceinline__ void ec_check(const EArgs& a, const PtSt& p, double t
     if (!(p.rho > 0.0) || !(th0 + p.th > 0.0)) atomicOr(a.flags, HEVI_F_EOS(a.stage));
 }
 
+// the same checks as flag bits, branch-free (accumulated over the sweep, one
+// atomic per thread at the end): x * 0 is NaN exactly for a non-finite x
+__device__ __forceinline__ unsigned ec_bits(const EArgs& a, const PtSt& p, double th0) {
+    const double z = fma(p.r, 0.0, fma(p.u, 0.0, fma(p.v, 0.0, fma(p.w, 0.0, p.th * 0.0))));
+    unsigned b = (z == z) ? 0u : HEVI_F_NONFINITE_IN(a.stage);
+    b |= (p.rho > 0.0 && th0 + p.th > 0.0) ? 0u : HEVI_F_EOS(a.stage);
+    return b;
+}
+
 // P' of a point from the per-level EOS constants (pprime of explicit_v2.cuh)
 __device__ __forceinline__ double ec_pprime(const EArgs& a, const LvlTab& lt, int gz, double r,
                                             double th) {
@@ -158,8 +167,9 @@ template <int MODE>
 __device__ __forceinline__ void ec_epilogue(const EArgs& a, const LvlTab& lt, long long o, int gz,
                                             const PtSt& p, const double (&Rv)[5], const double (&Lv)[5],
                                             const double (&Ai)[5], const double (&Fi)[5], bool bx,
-                                            bool by) {
+                                            bool by, bool own = true, unsigned* fl = nullptr) {
     const long long fs = a.g.fs;
+    if (!own) return;
     if (MODE == M_R) {
 #pragma unroll
         for (int f = 0; f < 5; ++f) a.out[o + f * fs] = Rv[f];
@@ -203,7 +213,8 @@ __device__ __forceinline__ void ec_epilogue(const EArgs& a, const LvlTab& lt, lo
             fin = fin && isfinite(qn[f]);
             a.out[o + f * fs] = qn[f];
         }
-        if (!fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
+        if (fl) *fl |= fin ? 0u : HEVI_F_NONFINITE_OUT;
+        else if (!fin) atomicOr(a.flags, HEVI_F_NONFINITE_OUT);
         // P' of the new state for the next step's stage 0 (replaces k_pp_plane)
         if (a.pp_out && fin) a.pp_out[o] = ec_pprime(a, lt, gz, qn[0], qn[4]);
     }
@@ -356,6 +367,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     __syncthreads();
 
     int k = 0;
+    unsigned fl = 0;   // flag bits of this thread's points (one atomic at the end)
     for (int l = 0; l < Z; ++l) {
         const bool top = (l == Z - 1);
         if (k == 0 && !top) {
@@ -436,8 +448,9 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
             for (int m = 1; m <= N; ++m) dz = fma(dzr[m], PLw[m], dz);
             ec_fold(6, 0.0, 0.0, fma(czf, car[6], dz), p, c);
         }
-        if (own) {
-            if (NEED_R) ec_check(a, p, lt.v[C_TH0][l]);
+        {
+            // every thread computes; only owned points store or raise flags
+            if (NEED_R) fl |= own ? ec_bits(a, p, lt.v[C_TH0][l]) : 0u;
             double Ai[5] = {0, 0, 0, 0, 0}, Fi[5] = {0, 0, 0, 0, 0};
             if (T::NAF) {
                 mbar_wait(&mbar[S + l % T::SAFM], (l / T::SAFM) & 1);
@@ -468,13 +481,15 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
                     so[(5 + f) * OX * OY] = qv[f] + a.cb * Rv[f];
                 }
                 const long long fs = g.fs;
-                a.P[o] = pr[0];
-                a.P[o + 3 * fs] = pr[3];
-                a.P[o + 4 * fs] = pr[4];
-                a.Quv[o + fs] = bx ? 0.0 : pr[1];
-                a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+                if (own) {
+                    a.P[o] = pr[0];
+                    a.P[o + 3 * fs] = pr[3];
+                    a.P[o + 4 * fs] = pr[4];
+                    a.Quv[o + fs] = bx ? 0.0 : pr[1];
+                    a.Quv[o + 2 * fs] = by ? 0.0 : pr[2];
+                }
             } else {
-                ec_epilogue<MODE>(a, lt, o, l, p, Rv, Lv, Ai, Fi, bx, by);
+                ec_epilogue<MODE>(a, lt, o, l, p, Rv, Lv, Ai, Fi, bx, by, own, &fl);
             }
         }
         if (l + 1 < Z) faces(l + 1, (l + 1) & 1);
@@ -501,6 +516,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
         }
         if (!top) k = (k + 1 == N) ? 0 : k + 1;
     }
+    if (fl) atomicOr(a.flags, fl);
     if (T::NOUT && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
