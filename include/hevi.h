@@ -230,6 +230,76 @@ int hevi_band_solve(const double *band, double *rhs, int n_col, int M, int nb, v
 /* max |a_i| over n doubles (device), deterministic */
 int hevi_absmax(const double *a, long long n, double *out_host, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * General curvilinear element meshes (the cubed-sphere shell,
+ * specgrid.build_cubed_sphere_mesh, specgrid.py:257-306): the same path on
+ * the reference's own E-vector layout (nf, nel, nq, nq, nq), nn = nel*nq^3
+ * nodes, node n = ((e*nq + k)*nq + j)*nq + i.  Vector fields are
+ * component-major [3][nn].  Columns have their own Schur factors
+ * (columnsolve.build_column_jacobian per column, :75-108).
+ * ------------------------------------------------------------------------- */
+typedef struct hevi_gplan hevi_gplan;
+
+/* host arrays, copied at creation (metric terms of specgrid.compute_metrics,
+ * :404-455; DSS groups of build_dss_map, :523-532; projectors of
+ * euler.boundary_projectors, :218-258; unique space of columnsolve.unique_space) */
+typedef struct {
+    int nel, N;
+    const double *D;                 /* (N+1)^2 LGL derivative, row-major      */
+    const double *ar, *as, *at;      /* contravariant a^r, a^s, a^t [3][nn]     */
+    const double *vert;              /* radial unit vector [3][nn]              */
+    const double *Jtv;               /* a^t . vert [nn]                         */
+    const double *w;                 /* wJ per node [nn]                        */
+    int n_groups;
+    const int *grp_ptr, *grp_idx;    /* CSR: members of each group, flat-node order */
+    const double *grp_wsum;          /* sum of wJ per group                     */
+    int n_proj;
+    const int *grp_slot;             /* per group: projector index or -1        */
+    const double *proj;              /* [n_proj][3][3] tangential projectors    */
+    int n_col, n_lev;
+    const int *uid;                  /* node -> col*n_lev + lev                 */
+    const int *rep;                  /* unique point -> first node              */
+} hevi_gmesh_desc;
+
+/* per-node background (euler.ReferenceState, euler.py:70-177) */
+typedef struct {
+    const double *rho0, *theta0, *P0f;       /* [nn]                  */
+    const double *grad_rho0, *grad_theta0;   /* [3][nn]               */
+    const double *gvec;                      /* g * vert [3][nn]      */
+    const double *G0, *H0;                   /* set2nc gamma P0f/rho0, gamma P0f/theta0 */
+    const double *F0vec;                     /* [3][nn] G0 grad rho0 + H0 grad theta0  */
+    const double *Theta0, *F0c;              /* set2c rho0 theta0, gamma P0f/Theta0     */
+    const double *Pb;                        /* EOS(rho0, theta0) [nn]                  */
+    double g, R, P0, gamma;
+    int eqset;                               /* 0 set2nc, 1 set2c */
+} hevi_gref_desc;
+
+int hevi_gplan_create(hevi_gplan **plan, const hevi_gmesh_desc *mesh, const hevi_gref_desc *ref);
+int hevi_gplan_destroy(hevi_gplan *plan);
+/* E-vectors of the plan's work area used by hevi_g_ark2_step / hevi_g_rk35_step */
+int hevi_g_work_fields(const hevi_gplan *plan);
+/* euler.nonlinear_rhs (euler.py:438-497) with DSS and no-flux projection */
+int hevi_g_rhs(hevi_gplan *plan, const double *q, double *R, void *stream);
+/* euler.vertical_restriction (euler.py:368-371) */
+int hevi_g_linear_v(hevi_gplan *plan, const double *q, double *L, void *stream);
+/* columnsolve.get_factors (factor_with_fallback): probe every column's
+ * vertical lhs_schur on the device, banded LU (pivoted dense fallback) */
+int hevi_g_factor(hevi_gplan *plan, double lam, int *nb_out, int *pivoted_out, void *stream);
+/* the probed (unfactored) matrix of column `col` into A_host (M x M); col < 0: all (n_col x M x M) */
+int hevi_g_column_matrix(hevi_gplan *plan, double lam, int col, double *A_host, void *stream);
+/* ImplicitProblem.solve direct (imexcore.py:312-322 -> columnsolve.solve_direct) */
+int hevi_g_solve(hevi_gplan *plan, double lam, const double *qe, double *q, void *stream);
+/* imexcore.ark_imex_step, ARK2 1D-IMEX direct, Q in place; work: hevi_g_work_fields E-vectors */
+int hevi_g_ark2_step(hevi_gplan *plan, double dt, const double *tab, double *Q, double *work, void *stream);
+/* imexcore.rk35_step, Q in place */
+int hevi_g_rk35_step(hevi_gplan *plan, double dt, double *Q, double *work, void *stream);
+/* specgrid.apply_dss_many on nf fields (in may equal out) */
+int hevi_g_dss(hevi_gplan *plan, const double *in, double *out, int nf, void *stream);
+/* Discretization.gradc / grad_vc (vertical_only): out [3][nn]; divc / div_vc: in [3][nn], out [nn] */
+int hevi_g_grad(hevi_gplan *plan, int vertical_only, const double *f, double *out, void *stream);
+int hevi_g_div(hevi_gplan *plan, int vertical_only, const double *vec, double *out, void *stream);
+int hevi_g_flags(hevi_gplan *plan, unsigned *flags, int reset, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,26 @@ class RefDesc(ctypes.Structure):
         (n, ctypes.c_double) for n in ("g", "R", "P0", "gamma")] + [("eqset", ctypes.c_int)]
 
 
+_IP = ctypes.POINTER(ctypes.c_int)
+
+
+class GMeshDesc(ctypes.Structure):
+    """hevi_gmesh_desc: general (curvilinear) mesh, host arrays."""
+    _fields_ = [("nel", ctypes.c_int), ("N", ctypes.c_int)] + [
+        (n, _DP) for n in ("D", "ar", "as_", "at", "vert", "Jtv", "w")] + [
+        ("n_groups", ctypes.c_int), ("grp_ptr", _IP), ("grp_idx", _IP), ("grp_wsum", _DP),
+        ("n_proj", ctypes.c_int), ("grp_slot", _IP), ("proj", _DP),
+        ("n_col", ctypes.c_int), ("n_lev", ctypes.c_int), ("uid", _IP), ("rep", _IP)]
+
+
+class GRefDesc(ctypes.Structure):
+    """hevi_gref_desc: per-node background."""
+    _fields_ = [(n, _DP) for n in (
+        "rho0", "theta0", "P0f", "grad_rho0", "grad_theta0", "gvec", "G0", "H0", "F0vec",
+        "Theta0", "F0c", "Pb")] + [
+        (n, ctypes.c_double) for n in ("g", "R", "P0", "gamma")] + [("eqset", ctypes.c_int)]
+
+
 # exported symbol -> (restype, argtypes); this list IS the C ABI of hevi.h
 _V = ctypes.c_void_p
 _I = ctypes.c_int
@@ -92,6 +112,21 @@ SIGNATURES = {
     "hevi_lu_pivot_solve": (_I, [_V, _V, _V, _I, _I, _V]),
     "hevi_plan_set_option": (_I, [_V, _I, _I]),
     "hevi_factor_pivoted": (_I, [_V, _D, ctypes.POINTER(_I)]),
+    # general (curvilinear) meshes: the cubed-sphere shell
+    "hevi_gplan_create": (_I, [ctypes.POINTER(_V), ctypes.POINTER(GMeshDesc), ctypes.POINTER(GRefDesc)]),
+    "hevi_gplan_destroy": (_I, [_V]),
+    "hevi_g_work_fields": (_I, [_V]),
+    "hevi_g_rhs": (_I, [_V, _V, _V, _V]),
+    "hevi_g_linear_v": (_I, [_V, _V, _V, _V]),
+    "hevi_g_factor": (_I, [_V, _D, ctypes.POINTER(_I), ctypes.POINTER(_I), _V]),
+    "hevi_g_column_matrix": (_I, [_V, _D, _I, _V, _V]),
+    "hevi_g_solve": (_I, [_V, _D, _V, _V, _V]),
+    "hevi_g_ark2_step": (_I, [_V, _D, _V, _V, _V, _V]),
+    "hevi_g_rk35_step": (_I, [_V, _D, _V, _V, _V]),
+    "hevi_g_dss": (_I, [_V, _V, _V, _I, _V]),
+    "hevi_g_grad": (_I, [_V, _I, _V, _V, _V]),
+    "hevi_g_div": (_I, [_V, _I, _V, _V, _V]),
+    "hevi_g_flags": (_I, [_V, ctypes.POINTER(ctypes.c_uint), _I, _V]),
 }
 
 _lib = None

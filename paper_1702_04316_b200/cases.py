@@ -58,3 +58,66 @@ def dt_for_courant(mesh, ref, q, courant, set_name="set2nc"):
     cmax = float(speed.max())
     _, dx_v = mesh.min_node_spacing()
     return courant * dx_v / cmax
+
+
+# ---------------------------------------------------------------------------
+# acoustic wave on the cubed-sphere shell (bench.py:23-105, cli.py:131-141)
+# ---------------------------------------------------------------------------
+
+class AcousticWaveConfig:
+    """bench.AcousticWaveConfig (bench.py:23-45): a cosine-bell pressure pulse
+    of amplitude dP with n_v vertical half-waves, centred at (lon0, lat0),
+    radius r_c on a shell [r_e, r_e + r_T]."""
+
+    def __init__(self, dP=100.0, n_v=1, r_e=6_371_000.0, r_T=10_000.0, r_c=None, lon0=0.0, lat0=0.0,
+                 theta0=300.0):
+        self.dP, self.n_v, self.r_e, self.r_T = dP, n_v, r_e, r_T
+        self.r_c = r_e / 3.0 if r_c is None else r_c
+        self.lon0, self.lat0, self.theta0 = lon0, lat0, theta0
+        if self.r_c > math.pi * self.r_e:
+            raise ValueError("perturbation radius exceeds the antipode")
+        if self.r_T <= 0:
+            raise ValueError("shell thickness must be positive")
+
+
+def init_acoustic_wave(cfg: AcousticWaveConfig, mesh, ref, set_name="set2nc", balance=True):
+    """bench.init_acoustic_wave (bench.py:78-120): P' = f(lon, lat) g(h), the
+    pulse put in hydrostatic balance (rho' = -(dP'/dh)/g, theta' from the
+    linearised EOS) or, with balance=False, pure density.  E-vector (numpy)."""
+    import numpy as np
+    from . import euler
+    c = mesh.coords
+    rad = np.linalg.norm(c, axis=-1)
+    lon = np.arctan2(c[..., 1], c[..., 0])
+    lat = np.arcsin(np.clip(c[..., 2] / rad, -1, 1))
+    cosang = math.sin(cfg.lat0) * np.sin(lat) + math.cos(cfg.lat0) * np.cos(lat) * np.cos(lon - cfg.lon0)
+    dist = cfg.r_e * np.arccos(np.clip(cosang, -1.0, 1.0))
+    f = np.where(dist <= cfg.r_c, 0.5 * cfg.dP * (1.0 + np.cos(np.pi * dist / cfg.r_c)), 0.0)
+    m = cfg.n_v * np.pi / cfg.r_T
+    Pp = f * np.sin(m * mesh.height)
+    q = np.zeros((5,) + tuple(mesh.nshape))
+    if balance:
+        rho_p = -f * m * np.cos(m * mesh.height) / euler.GasConstants().g
+        th_p = (Pp - ref.G0_nc * rho_p) / ref.H0_nc
+    else:
+        rho_p = Pp / ref.G0_nc
+        th_p = np.zeros_like(rho_p)
+    q[0] = rho_p
+    q[4] = ref.theta0 * rho_p + ref.rho0 * th_p if set_name == "set2c" else th_p
+    return q
+
+
+def probe_point_on_sphere(cfg: AcousticWaveConfig, angle_rad: float, height: float):
+    """bench.probe_point_on_sphere (bench.py:177-185): great-circle angle east
+    of the source at a height above r_e."""
+    lon = cfg.lon0 + angle_rad
+    r = cfg.r_e + height
+    return (r * math.cos(cfg.lat0) * math.cos(lon), r * math.cos(cfg.lat0) * math.sin(lon),
+            r * math.sin(cfg.lat0))
+
+
+def nearest_node(mesh, point) -> int:
+    """bench.nearest_node (bench.py:171-174): flat node index nearest a point."""
+    import numpy as np
+    d = np.linalg.norm(mesh.coords.reshape(-1, 3) - np.asarray(point), axis=1)
+    return int(np.argmin(d))

@@ -137,6 +137,15 @@ def build_column_jacobian(problem) -> ColumnJacobian:
     plan = problem.disc.plan_for(problem.ref, problem.set_name)
     lam = float(problem.lam)
     space = unique_space(problem.disc.mesh)
+    if getattr(problem.disc.mesh, "kind", "box") == "sphere":
+        # general mesh: every column probed on the device (leakage check included)
+        if lam == 0.0:
+            mats = torch.eye(space.n_lev, dtype=torch.float64, device=plan.device).expand(
+                space.n_col, -1, -1).contiguous()
+            return ColumnJacobian(matrices=mats, bandwidth=1, n_dof=1, space=space, pivoted_fallback=[], piv={})
+        nb, _ = plan.factor(lam)
+        mats = torch.as_tensor(plan.column_matrix(lam, -1), device=plan.device)
+        return ColumnJacobian(matrices=mats, bandwidth=nb, n_dof=1, space=space, pivoted_fallback=[], piv={})
     if lam == 0.0:
         A = np.eye(space.n_lev)
         nb = 1

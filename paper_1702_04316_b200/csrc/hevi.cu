@@ -1192,6 +1192,7 @@ __global__ void k_absmax(const double* a, long long n, unsigned long long* out) 
 #include "explicit_c.cuh"
 #include "solve_v2.cuh"
 #include "imex3d.cuh"
+#include "general.cuh"
 
 // P' plane of a lattice state over the plan's whole window (stage 0 of the
 // fused step: formed once per point here instead of for every staged,
@@ -1279,6 +1280,35 @@ struct hevi_plan {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double* ppscratch = nullptr;   // hevi_rhs on the column sweep: P'(q) of the caller's state
     LvlTab lt;               // per-level constants of the explicit_col kernels
+};
+
+// general (curvilinear) mesh plan: per-column Schur factors
+struct GFactor {
+    double lam = 0.0;
+    int nb = 0, pivoted = 0;
+    double* A = nullptr;      // n_col x M x M probed matrices (kept for hevi_g_column_matrix)
+    double* band = nullptr;   // n_col x M x (2nb-1) no-pivot banded LU (k_band_* layout)
+    double* LUP = nullptr;    // pivoted dense LU per column (fallback)
+    int* piv = nullptr;
+};
+
+struct hevi_gplan {
+    GGeo g;
+    GRef r;
+    long long nn = 0;
+    int n_groups = 0, n_proj = 0, n_col = 0, n_lev = 0;
+    int *d_gptr = nullptr, *d_gidx = nullptr, *d_gslot = nullptr, *d_uid = nullptr, *d_rep = nullptr,
+        *d_bslot = nullptr;
+    double *d_w = nullptr, *d_wsum = nullptr;
+    double* d_arr = nullptr;   // geometry and background arrays
+    double* d_scr = nullptr;   // scratch: s0, s1, ua[3], up[3], sP, sO
+    double *s0 = nullptr, *s1 = nullptr, *ua = nullptr, *up = nullptr, *sP = nullptr, *sO = nullptr;
+    double* col = nullptr;     // n_col x n_lev column buffer
+    unsigned* d_flags = nullptr;
+    unsigned* h_flags = nullptr;
+    unsigned long long* d_bits = nullptr;
+    int* d_nb = nullptr;
+    std::map<long long, GFactor> factors;
 };
 
 namespace {
@@ -1939,6 +1969,8 @@ int blocks_for(long long n, int T = 256) {
     if (b < 1) b = 1;
     return (int)b;
 }
+
+#include "general_host.cuh"
 
 }  // namespace
 
@@ -2740,5 +2772,7 @@ int hevi_absmax(const double* a, long long n, double* out_host, void* stream) {
     *out_host = v;
     return HEVI_OK;
 }
+
+#include "general_api.cuh"
 
 }  // extern "C"

@@ -128,7 +128,7 @@ __host__ __device__ constexpr size_t s2_smem_bytes(int M, int T) {
 template <int N, bool SC>   // SC: conservative set set2c
 __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     using R = S2Rec<N>;
-    constexpr int W = 4 * N + 1, RS = R::RS;
+    constexpr int RS = R::RS;
     extern __shared__ __align__(16) double sm2[];
     const Geo& g = a.g;
     const int M = g.Z;

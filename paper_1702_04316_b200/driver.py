@@ -13,8 +13,10 @@ operators; diagnostics are one device reduction per record
 snapshot.  Supported: box meshes (``case = bubble | rest-state``), cG,
 ``set2nc``/``set2c``, ``integrator = rk35``, and ARK2 / BDF2 with the Schur
 form: ``imex = 1d, solver = direct`` (fused column solve) or the Krylov
-solvers on either form (``imex = 1d | 3d``).  The cubed-sphere acoustic case,
-dG and the standard (5-variable) form raise ``NotImplementedError``.
+solvers on either form (``imex = 1d | 3d``); the cubed-sphere acoustic case
+(``case = acoustic``: the general-mesh plan of ``sphere``, E-vector state,
+ARK2 / BDF2 with ``imex = 1d, solver = direct`` and per-column factors, or
+RK35).  dG and the standard (5-variable) form raise ``NotImplementedError``.
 
     python -m paper_1702_04316_b200.driver run <config> [--key=value ...]
 """
@@ -120,8 +122,9 @@ def parse_config(path=None, overrides=()) -> RunConfig:
 
 
 def _check_supported(cfg: RunConfig):
-    if cfg.case == "acoustic":
-        raise NotImplementedError("the cubed-sphere acoustic case is outside the box-mesh path")
+    if cfg.case == "acoustic" and cfg.integrator in ("ark2", "bdf2") and cfg.solver != "direct":
+        raise NotImplementedError("on the cubed-sphere shell the device path runs the 1D-IMEX "
+                                  "direct solve (imex=1d, solver=direct) and RK35")
     if cfg.disc != "cg":
         raise NotImplementedError("dG is outside the HEVI direct path")
     if cfg.integrator in ("ark2", "bdf2") and cfg.form != "schur":
@@ -283,6 +286,8 @@ def run_simulation(cfg: RunConfig, quiet=False) -> RunResult:
     from .plan import tableau_array
     _check_supported(cfg)
     os.makedirs(cfg.output_dir, exist_ok=True)
+    if cfg.case == "acoustic":
+        return _run_sphere(cfg, quiet)
     mesh, ref, disc, Q0, probe_xyz = _build_case(cfg)
     set_name = cfg.equation_set
     rho = torch.as_tensor(ref.rho0, device=Q0.device)[:, None, None] + Q0[0]
@@ -395,6 +400,127 @@ def run_simulation(cfg: RunConfig, quiet=False) -> RunResult:
     return RunResult(steps=steps, wall_time=wall, dt=dt, courant_h=ch, courant_v=cv,
                      stats=stats, diagnostics=diags, final_q=q, exit_code=exit_code,
                      message=message)
+
+
+def write_snapshot_nodes(path, t, q, mesh, ref, set_name):
+    """cli.write_snapshot (cli.py:157-170) with a per-node background (general meshes)."""
+    q = q.cpu().numpy() if hasattr(q, "cpu") else np.asarray(q)
+    vel = np.moveaxis(q[1:4], 0, -1)
+    if set_name == "set2c":
+        rho = ref.rho0 + q[0]
+        vel = vel / rho[..., None]
+        th_p = (ref.Theta0 + q[4]) / rho - ref.theta0
+    else:
+        th_p = q[4]
+    xyz = mesh.coords.reshape(-1, 3)
+    data = np.column_stack([xyz, q[0].reshape(-1), vel.reshape(-1, 3), th_p.reshape(-1)])
+    np.savetxt(path, data, fmt="%.10g", header=f"time={t:.10g} fields=x y z rho_p u v w theta_p")
+
+
+def _run_sphere(cfg: RunConfig, quiet=False) -> RunResult:
+    """The acoustic case on the cubed-sphere shell (cli.py:131-141, 173-263):
+    E-vector state on the device, the general-mesh plan (sphere.GPlan):
+    ARK2 1D-IMEX direct with per-column factors, or RK35."""
+    import torch
+    from .plan import tableau_array
+    acfg = cases.AcousticWaveConfig(theta0=cfg.theta0)
+    mesh = sg.build_cubed_sphere_mesh(cfg.ne_panel, cfg.ne_vert, acfg.r_e, acfg.r_T, cfg.order)
+    const = euler.GasConstants()
+    # constant-temperature background: uniform sound speed (cli.py:136-138)
+    ref = euler.isothermal_reference(mesh, cfg.theta0, const)
+    set_name = cfg.equation_set
+    q0 = cases.init_acoustic_wave(acfg, mesh, ref, set_name)
+    if np.any(ref.rho0 + q0[0] <= 0):
+        raise FloatingPointError("total density lost positivity")
+    disc = euler.build_discretization(mesh)
+    plan = disc.plan_for(ref, set_name)
+    Q = plan.dss(torch.as_tensor(q0, device=plan.device))   # coincident copies consistent (cli.py:180)
+    work = plan.workspace()
+    dx_h, dx_v = euler.min_node_spacing(mesh)
+    _, cv0 = euler.courant_numbers(Q, ref, disc, 1.0, set_name)
+    dt = cfg.dt if cfg.dt > 0 else cfg.courant * dx_v / (cv0 * dx_v)
+    ch, cv = euler.courant_numbers(Q, ref, disc, dt, set_name)
+    problem = None
+    if cfg.integrator in ("ark2", "bdf2"):
+        problem = imexcore.ImplicitProblem(
+            disc=disc, ref=ref, set_name=set_name, discretization=cfg.disc, form=cfg.form,
+            dim="1d" if cfg.imex == "1d" else "3d",
+            solver=imexcore.SolverSpec(method=cfg.solver, tol=cfg.tolerance, precon_order=cfg.precon_order))
+    ark = imexcore.ark2_tableau()
+    tarr = tableau_array(ark)
+    bdf = imexcore.bdf2_coefficients()
+    rhs = euler.make_rhs(ref, disc, set_name)
+    wJ = torch.as_tensor(disc.metrics.wJ, device=plan.device)
+    rho0 = torch.as_tensor(ref.rho0, device=plan.device)
+    pid = cases.nearest_node(mesh, cases.probe_point_on_sphere(acfg, np.pi / 2, 0.0))
+    if set_name == "set2nc":
+        pc = (float(ref.G0_nc.ravel()[pid]), float(ref.H0_nc.ravel()[pid]))
+    else:
+        pc = (0.0, float(ref.F0_c.ravel()[pid]))
+    diags = Diagnostics()
+
+    def record(t):
+        mass = float((wJ * (rho0 + Q[0])).sum())
+        v = Q[[0, 4]].reshape(2, -1)[:, pid].cpu().numpy()
+        diags.record_values(t, mass, float(Q[0].abs().max()), float(Q[4].abs().max()),
+                            (pc[0] * v[0] + pc[1] * v[1],))
+
+    t, steps = 0.0, 0
+    record(t)
+    next_diag = cfg.diag_interval
+    q_prev = None
+    Qgood = torch.empty_like(Q)
+    inplace = False
+    t0 = time.perf_counter()
+    exit_code, message = 0, ""
+    try:
+        while t < cfg.end_time - 1e-12:
+            step_dt = min(dt, cfg.end_time - t)
+            Qgood.copy_(Q)
+            if cfg.integrator == "rk35":
+                inplace = True
+                plan.rk35(step_dt, Q, work)
+                plan.check_flags()
+                inplace = False
+            elif cfg.integrator == "ark2" or q_prev is None or step_dt != dt:
+                if cfg.integrator == "bdf2":
+                    q_prev = Q.clone()
+                problem.lam = ark.diag * step_dt
+                inplace = True
+                plan.step(step_dt, tarr, Q, work)
+                plan.check_flags()
+                inplace = False
+                problem.stats.solves += 2
+            else:
+                qn = Q.clone()
+                Q.copy_(imexcore.bdf2_imex_step(qn, q_prev, step_dt, bdf, problem, rhs))
+                q_prev = qn
+            t += step_dt
+            steps += 1
+            if cfg.diag_interval <= 0 or t >= next_diag - 1e-12:
+                record(t)
+                next_diag += cfg.diag_interval
+    except imexcore.SolverFailure as exc:
+        exit_code, message = 3, str(exc)
+    except FloatingPointError as exc:
+        exit_code, message = 4, str(exc)
+    finally:
+        if inplace:
+            Q.copy_(Qgood)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    diags.write_csv(os.path.join(cfg.output_dir, "timeseries.csv"))
+    snap = os.path.join(cfg.output_dir, f"snapshot_{t:012.3f}.txt")
+    write_snapshot_nodes(snap, t, Q, mesh, ref, set_name)
+    stats = problem.stats if problem is not None else imexcore.SolveStats()
+    if not quiet:
+        mean_it = stats.iterations / max(stats.solves, 1)
+        print(f"steps={steps} wall={wall:.3f}s dt={dt:.6g} C_H={ch:.3g} C_V={cv:.3g} "
+              f"solves={stats.solves} mean_iters={mean_it:.2f} matvecs={stats.matvecs}")
+        if message:
+            print(f"aborted: {message} (last snapshot: {snap})")
+    return RunResult(steps=steps, wall_time=wall, dt=dt, courant_h=ch, courant_v=cv, stats=stats,
+                     diagnostics=diags, final_q=Q.cpu().numpy(), exit_code=exit_code, message=message)
 
 
 def main(argv=None) -> int:

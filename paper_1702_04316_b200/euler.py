@@ -148,6 +148,9 @@ def _level_heights(mesh: sg.BoxMesh) -> np.ndarray:
 def hydrostatic_reference(mesh: sg.BoxMesh, theta_bg: float,
                           const: GasConstants = GasConstants()) -> ReferenceState:
     """Constant-theta hydrostatic background (euler.py:125-150)."""
+    if _general(mesh):
+        from . import sphere
+        return sphere.hydrostatic_reference(mesh, theta_bg, const)
     if theta_bg <= 0:
         raise ValueError("background potential temperature must be positive")
     c = const
@@ -167,6 +170,9 @@ def hydrostatic_reference(mesh: sg.BoxMesh, theta_bg: float,
 def isothermal_reference(mesh: sg.BoxMesh, T_bg: float,
                          const: GasConstants = GasConstants()) -> ReferenceState:
     """Constant-temperature hydrostatic background (euler.py:153-177)."""
+    if _general(mesh):
+        from . import sphere
+        return sphere.isothermal_reference(mesh, T_bg, const)
     if T_bg <= 0:
         raise ValueError("background temperature must be positive")
     c = const
@@ -179,6 +185,11 @@ def isothermal_reference(mesh: sg.BoxMesh, T_bg: float,
     dth0 = (c.g / c.c_p) / pi
     return ReferenceState(const=c, kind="isothermal", height=h, rho0=rho0, theta0=theta0,
                           P0f=P0f, drho0=drho0, dtheta0=dth0, mesh=mesh)
+
+
+def _general(mesh) -> bool:
+    """A general curvilinear mesh (the cubed-sphere shell), not the box."""
+    return getattr(mesh, "kind", "box") == "sphere"
 
 
 def _node_levels(mesh):
@@ -197,6 +208,16 @@ def linearized_pressure(q, ref: ReferenceState, set_name: str, mesh: sg.BoxMesh 
     (host/diagnostic helper: the kernels form it inline)."""
     if set_name not in ("set2nc", "set2c"):
         raise ValueError(f"unknown equation set {set_name!r}")
+    if not isinstance(ref, ReferenceState):     # per-node background (general mesh)
+        import torch
+        from .plan import to_device
+        E, back = to_device(q)
+
+        def node(a):
+            return torch.as_tensor(np.asarray(a), device=E.device)
+        if set_name == "set2nc":
+            return back(node(ref.G0_nc) * E[0] + node(ref.H0_nc) * E[4])
+        return back(node(ref.F0_c) * E[4])
     mesh = mesh if mesh is not None else ref.mesh
     if mesh is None:
         raise ValueError("linearized_pressure needs the mesh the ReferenceState was built on")
@@ -324,7 +345,11 @@ class _BoxMetrics:
 
 
 def build_discretization(mesh: sg.BoxMesh) -> Discretization:
-    """Metric/DSS set-up (euler.py:303-310) for the structured box."""
+    """Metric/DSS set-up (euler.py:303-310): the structured box, or a general
+    curvilinear mesh (the cubed-sphere shell, ``sphere``)."""
+    if _general(mesh):
+        from . import sphere
+        return sphere.build_discretization(mesh)
     if not isinstance(mesh, sg.BoxMesh):
         raise TypeError("the B200 HEVI path supports structured box meshes "
                         "(specgrid.build_box_mesh / build_box_mesh_3d)")
@@ -339,7 +364,11 @@ def boundary_projectors(mesh: sg.BoxMesh, metrics=None, dss=None):
     box: every E-vector node on a domain face with the tangential projector
     I - sum n n^T over the (orthonormal, axis-aligned) normals meeting there.
     Lateral x faces, the slab's y faces (its dummy layer), lateral y faces
-    (3D) and the bottom/top faces."""
+    (3D) and the bottom/top faces.  General meshes: the face normals
+    gathered through the coincidence groups (``sphere.boundary_projectors``)."""
+    if _general(mesh):
+        from . import sphere
+        return sphere.boundary_projectors(mesh, metrics, dss)[:2]
     nel, nt, ns, nr = mesh.nshape
     e = np.arange(nel)
     kx = e % mesh.nx
@@ -379,6 +408,9 @@ def zero_normal_velocity(vel, bidx, bproj):
 
 def min_node_spacing(mesh: sg.BoxMesh):
     """Minimal horizontal / vertical internodal distances (euler.py:583-593)."""
+    if _general(mesh):
+        from . import sphere
+        return sphere.min_node_spacing(mesh)
     return mesh.min_node_spacing()
 
 

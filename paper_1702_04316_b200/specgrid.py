@@ -292,13 +292,16 @@ def build_dss_map(mesh: BoxMesh, plan_getter=None) -> BoxDss:
 def apply_dss_many(fields, dss: BoxDss):
     """DSS along the leading axis of stacked E-vector fields (specgrid.py:543-548):
     every coincident copy takes the mass-weighted average of all copies, on
-    the device (``hevi_dss``).  numpy in -> numpy out, torch in -> torch out."""
+    the device (``hevi_dss``; general meshes: ``hevi_g_dss``).  numpy in ->
+    numpy out, torch in -> torch out."""
     from . import _native as nv
     from .plan import to_device
     import torch
     E, back = to_device(fields)
-    if tuple(E.shape[1:]) != dss.shape:
+    if tuple(E.shape[1:]) != tuple(dss.shape):
         raise ValueError("field/DSS map shape mismatch")
+    if not isinstance(dss, BoxDss):      # sphere.GroupMap
+        return back(dss.disc.geometry_plan().dss(E))
     plan = dss.plan()
     out = torch.empty_like(E)
     wx, wy, wz = dss.device_tables(E.device)
@@ -309,6 +312,13 @@ def apply_dss_many(fields, dss: BoxDss):
 
 def apply_dss(f, dss: BoxDss):
     """Replace coincident-node values by their mass-weighted average (specgrid.py:535-540)."""
-    if tuple(f.shape) != dss.shape:
+    if tuple(f.shape) != tuple(dss.shape):
         raise ValueError("field/DSS map shape mismatch")
     return apply_dss_many(f[None], dss)[0]
+
+
+def build_cubed_sphere_mesh(ne_panel: int, ne_vert: int, r_e: float, r_T: float, N: int):
+    """Equiangular gnomonic cubed-sphere shell (specgrid.py:257-306); the
+    general-mesh path of ``sphere``."""
+    from .sphere import build_cubed_sphere_mesh as build
+    return build(ne_panel, ne_vert, r_e, r_T, N)

@@ -34,11 +34,22 @@ CASES = {
                 "--nx=4", "--nz=4", "--courant=2", "--end_time=0.6"],
     "bdf2_3d_bicg": ["--integrator=bdf2", "--imex=3d", "--solver=bicgstab", "--precon_order=3",
                      "--tolerance=1e-10", "--nx=4", "--nz=4", "--courant=2", "--end_time=0.8"],
+    # the cubed-sphere acoustic case (cli.py:131-141)
+    "acoustic_ark2": ["--case=acoustic", "--integrator=ark2", "--imex=1d", "--solver=direct",
+                      "--ne_panel=2", "--ne_vert=2", "--order=3", "--courant=4", "--end_time=60"],
+    "acoustic_rk35": ["--case=acoustic", "--integrator=rk35", "--ne_panel=2", "--ne_vert=1",
+                      "--order=3", "--courant=0.5", "--end_time=4"],
+    "acoustic_bdf2_c": ["--case=acoustic", "--integrator=bdf2", "--imex=1d", "--solver=direct",
+                        "--equation_set=set2c", "--ne_panel=2", "--ne_vert=2", "--order=3",
+                        "--courant=4", "--end_time=60"],
 }
 
 
 def main():
+    only = set(sys.argv[1:])
     for name, ov in CASES.items():
+        if only and name not in only:
+            continue
         with tempfile.TemporaryDirectory() as d:
             cfg = cli.parse_config(None, ov + [f"--output_dir={d}"])
             res = cli.run_simulation(cfg, quiet=True)

@@ -19,7 +19,8 @@ def load(name):
     return np.load(os.path.join(HERE, "golden", f"driver_{name}.npz"))
 
 
-@pytest.mark.parametrize("name", ["ark2", "rk35", "bdf2_c", "ark2_rest", "ark2_3d", "bdf2_3d_bicg"])
+@pytest.mark.parametrize("name", ["ark2", "rk35", "bdf2_c", "ark2_rest", "ark2_3d", "bdf2_3d_bicg",
+                                  "acoustic_ark2", "acoustic_rk35", "acoustic_bdf2_c"])
 def test_run_matches_reference_driver(name, tmp_path):
     g = load(name)
     cfg = driver.parse_config(None, list(g["overrides"]) + [f"--output_dir={tmp_path}"])
