@@ -113,9 +113,19 @@ int hevi_ark2_step(hevi_plan *plan, double dt, const double *tab, double *Q, dou
 #define HEVI_STEP_PP_VALID 1u
 int hevi_ark2_step_ex(hevi_plan *plan, double dt, const double *tab, double *Q, double *work,
                       unsigned flags, void *stream);
-/* hevi_stage with the HEVI_STEP_PP_VALID contract of hevi_ark2_step_ex (stage 0) */
+/* hevi_stage with the HEVI_STEP_PP_VALID contract of hevi_ark2_step_ex (stage 0)
+ * and, for partitioned runs, the tile subset: HEVI_STAGE_INTERIOR evaluates
+ * only the tiles that read no halo point a neighbour rank provides (it may
+ * run while the halo exchange is in flight), HEVI_STAGE_BOUNDARY the rest
+ * and the domain-end planes (after the exchange); the two calls together
+ * are the stage, bitwise.  Paths without the tile split do the whole stage
+ * in the boundary call. */
+#define HEVI_STAGE_INTERIOR 2u
+#define HEVI_STAGE_BOUNDARY 4u
 int hevi_stage_ex(hevi_plan *plan, int stage, double dt, const double *tab,
                   double *Q, double *work, unsigned flags, void *stream);
+/* tiles of the column-sweep stage kernels in the interior / boundary subsets */
+int hevi_stage_tiles(const hevi_plan *plan, int *n_interior, int *n_boundary);
 /* P'(Q) into work's Q1 field 0 (the plane the chained step reads) */
 int hevi_pp_refresh(hevi_plan *plan, const double *Q, double *work, void *stream);
 /* 1 if hevi_ark2_step_ex writes P'(Q^{n+1}) for the next step on this plan */

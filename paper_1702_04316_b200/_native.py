@@ -17,6 +17,8 @@ F_NONFINITE_OUT = 1 << 12
 F_PIVOT = 1 << 13
 F_AINV = 1 << 14
 STEP_PP_VALID = 1
+STAGE_INTERIOR = 2
+STAGE_BOUNDARY = 4
 
 
 def F_NONFINITE_IN(stage):
@@ -85,6 +87,7 @@ SIGNATURES = {
     "hevi_pp_refresh": (_I, [_V, _V, _V, _V]),
     "hevi_stage_ex": (_I, [_V, _I, _D, _V, _V, _V, ctypes.c_uint, _V]),
     "hevi_step_chains_pp": (_I, [_V]),
+    "hevi_stage_tiles": (_I, [_V, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "hevi_rk35_step": (_I, [_V, _D, _V, _V, _V]),
     "hevi_evec_to_lattice": (_I, [_V, _V, _V, _I, _V]),
     "hevi_lattice_to_evec": (_I, [_V, _V, _V, _I, _V]),

@@ -47,6 +47,36 @@ struct LvlTab {
     double cg[EC_ZMAX][5], ch[EC_ZMAX][5];   // Dz[N][m] * G0 / H0 [l + m]: row-N carry of P_lin, layer base l
 };
 
+// the tile of this CTA (EArgs::tmode): the whole grid, the interior
+// rectangle, or the i-th tile of the ring around it (bottom rows, top rows,
+// then the left / right tiles of the middle rows)
+__device__ __forceinline__ void ec_tile(const EArgs& a, int& bx, int& by) {
+    if (a.tmode == 0) {
+        bx = blockIdx.x;
+        by = blockIdx.y;
+    } else if (a.tmode == 1) {
+        bx = a.tb[2] + blockIdx.x;
+        by = a.tb[4] + blockIdx.y;
+    } else {
+        const int nbx = a.tb[0], nby = a.tb[1], bx0 = a.tb[2], bx1 = a.tb[3], by0 = a.tb[4], by1 = a.tb[5];
+        int i = blockIdx.x;
+        const int nlow = by0 * nbx, nhigh = (nby - by1) * nbx;
+        if (i < nlow) {
+            by = i / nbx;
+            bx = i % nbx;
+        } else if ((i -= nlow) < nhigh) {
+            by = by1 + i / nbx;
+            bx = i % nbx;
+        } else {
+            i -= nhigh;
+            const int wl = bx0, w = bx0 + (nbx - bx1);
+            by = by0 + i / w;
+            const int r = i % w;
+            bx = r < wl ? r : bx1 + (r - wl);
+        }
+    }
+}
+
 // TMA bulk tensor store of one staged box (shared::cta -> global)
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
     asm volatile(
@@ -248,7 +278,9 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
     const int Z = g.Z;
     const int tid = threadIdx.x;
     const int ox = tid % OX, oy = tid / OX;
-    const int ex0 = g.ex_b + blockIdx.x * TX, ey0 = g.ey_b + blockIdx.y * TY;
+    int bxt, byt;
+    ec_tile(a, bxt, byt);
+    const int ex0 = g.ex_b + bxt * TX, ey0 = g.ey_b + byt * TY;
     const int gx = ex0 * N + ox, gy = ey0 * N + oy;
     const bool own = gx < g.ex_e * N && gy < g.ey_e * N;
     const int tx0 = (ex0 - 1) * N - g.x0, ty0 = (ey0 - 1) * N - g.y0;

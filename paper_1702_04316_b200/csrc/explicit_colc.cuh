@@ -134,7 +134,9 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
     const int Z = g.Z;
     const int tid = threadIdx.x;
     const int ox = tid % OX, oy = tid / OX;
-    const int ex0 = g.ex_b + blockIdx.x * TX, ey0 = g.ey_b + blockIdx.y * TY;
+    int bxt, byt;
+    ec_tile(a, bxt, byt);
+    const int ex0 = g.ex_b + bxt * TX, ey0 = g.ey_b + byt * TY;
     const int gx = ex0 * N + ox, gy = ey0 * N + oy;
     const bool own = gx < g.ex_e * N && gy < g.ey_e * N;
     const int tx0 = (ex0 - 1) * N - g.x0, ty0 = (ey0 - 1) * N - g.y0;

@@ -116,6 +116,11 @@ struct EArgs {
     const double* pp_in;   // M_S2/M_S3 (set2nc): P' plane of the stage input from the column solve
     double* pp_out;        // explicit_col M_S3: P' plane of the new state (next step's stage 0)
     unsigned long long* dbg;   // HEVI_PHASE_TIMING builds: per-phase clock64 sums
+    // tile subset of the column-sweep kernels (hevi_stage_ex HEVI_STAGE_*):
+    // 0 every tile; 1 the interior rectangle [tb2, tb3) x [tb4, tb5); 2 the
+    // ring of tiles around it (tb0 x tb1 tiles in all)
+    int tmode;
+    int tb[6];
 };
 
 struct SArgs {
@@ -1627,9 +1632,38 @@ int make_tmap_fields(CUtensorMap* m, const Geo& g, const double* base, int bx, i
     return HEVI_OK;
 }
 
+// tile split of a rank window for overlapping the halo exchange with the
+// sweep: a tile is on the ring when its staged box reaches a halo point a
+// neighbour rank provides (low side: the first tile when ex_b > 0; high
+// side: the last tile when ex_e < nex; the same in y); the rest is interior
+void tile_split(const Geo& g, int TX, int TY, int tb[6]) {
+    const int nbx = (g.ex_e - g.ex_b + TX - 1) / TX, nby = (g.ey_e - g.ey_b + TY - 1) / TY;
+    const int bx0 = g.ex_b > 0 ? 1 : 0, by0 = g.ey_b > 0 ? 1 : 0;
+    int bx1 = nbx - (g.ex_e < g.nex ? 1 : 0), by1 = nby - (g.ey_e < g.ney ? 1 : 0);
+    if (bx1 < bx0) bx1 = bx0;
+    if (by1 < by0) by1 = by0;
+    tb[0] = nbx;
+    tb[1] = nby;
+    tb[2] = bx0;
+    tb[3] = bx1;
+    tb[4] = by0;
+    tb[5] = by1;
+}
+
+// grid of the column-sweep launch for the tile subset of a.tmode (0 tiles: no launch)
+dim3 tile_grid(EArgs& a, const Geo& g, int TX, int TY) {
+    if (a.tmode == 0) return dim3((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
+    tile_split(g, TX, TY, a.tb);
+    const int ni = (a.tb[3] - a.tb[2]) * (a.tb[5] - a.tb[4]);
+    if (a.tmode == 1) return ni ? dim3(a.tb[3] - a.tb[2], a.tb[5] - a.tb[4]) : dim3(0, 0);
+    const int nr = a.tb[0] * a.tb[1] - ni;
+    return dim3(nr, nr ? 1 : 0);
+}
+
 template <int N, int MODE>
-int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
+int launch_col(const hevi_plan* pl, const EArgs& a0, cudaStream_t st) {
     using T = EC<N, MODE>;
+    EArgs a = a0;
     const Geo& g = pl->g;
     static size_t attr[16] = {0};
     auto kern = k_ecol<N, MODE>;
@@ -1656,12 +1690,15 @@ int launch_col(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     // the domain-end plane: the edge kernel must then run after the sweep
     const bool partial_end = ((g.ex_e == g.nex) && (g.ex_e - g.ex_b) % T::TX != 0) ||
                              ((g.ey_e == g.ney) && (g.ey_e - g.ey_b) % T::TY != 0);
-    const bool fork = npt > 0 && pl->side != nullptr && !(T::NOUT && partial_end);
+    const dim3 grid = tile_grid(a, g, T::TX, T::TY);
+    const bool edge = npt > 0 && a.tmode != 1;   // the interior subset has no domain-end plane
+    const bool fork = edge && pl->side != nullptr && !(T::NOUT && partial_end);
     if (fork) CK(cudaEventRecord(pl->ev_fork, st));
-    const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
-    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF, o0, o1, o2, o3);
-    CK(cudaGetLastError());
-    if (npt > 0) {
+    if (grid.x && grid.y) {
+        kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF, o0, o1, o2, o3);
+        CK(cudaGetLastError());
+    }
+    if (edge) {
         // launched after the sweep: its blocks are dispatched as the sweep's last CTAs retire
         cudaStream_t es = fork ? pl->side : st;
         if (fork) CK(cudaStreamWaitEvent(es, pl->ev_fork, 0));
@@ -1696,12 +1733,15 @@ int launch_colc(const hevi_plan* pl, const EArgs& a0, cudaStream_t st) {
     const int nxc = (g.ex_e == g.nex) ? (g.ey_e - g.ey_b) * N + (g.ey_e == g.ney ? 1 : 0) : 0;
     const int nyr = (g.ey_e == g.ney) ? (g.ex_e - g.ex_b) * N : 0;
     const long long npt = (long long)(nxc + nyr) * g.Z;
-    const bool fork = npt > 0 && pl->side != nullptr;
+    const dim3 grid = tile_grid(a, g, T::TX, T::TY);
+    const bool edge = npt > 0 && a.tmode != 1;
+    const bool fork = edge && pl->side != nullptr;
     if (fork) CK(cudaEventRecord(pl->ev_fork, st));
-    const dim3 grid((g.ex_e - g.ex_b + T::TX - 1) / T::TX, (g.ey_e - g.ey_b + T::TY - 1) / T::TY);
-    kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tA, tF);
-    CK(cudaGetLastError());
-    if (npt > 0) {
+    if (grid.x && grid.y) {
+        kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tA, tF);
+        CK(cudaGetLastError());
+    }
+    if (edge) {
         cudaStream_t es = fork ? pl->side : st;
         if (fork) CK(cudaStreamWaitEvent(es, pl->ev_fork, 0));
         k_ecolc_edge<N, MODE><<<(unsigned)((npt + 127) / 128), 128, 0, es>>>(a, pl->lt, nxc, nyr, g.ex_b * N,
@@ -1743,6 +1783,13 @@ int run_col(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
 }
 
 int run_e(const hevi_plan* pl, int mode, const EArgs& a, cudaStream_t st) {
+    if (a.tmode && !colc_applies(pl, mode) && !(pl->eqset == 0 && col_applies(pl, mode, a))) {
+        // no tile split on this path: the boundary call does the whole stage
+        if (a.tmode == 1) return HEVI_OK;
+        EArgs b = a;
+        b.tmode = 0;
+        return run_e(pl, mode, b, st);
+    }
     if (colc_applies(pl, mode)) return run_colc(pl, mode, a, st);
     if (pl->eqset == 1) {
         switch (mode) {
@@ -2310,7 +2357,7 @@ int hevi_pp_refresh(hevi_plan* pl, const double* Q, double* work, void* stream) 
 }
 
 static int stage_impl(hevi_plan* pl, int stage, double dt, const double* tab, double* Q, double* work,
-                      bool pp_chain, void* stream) {
+                      bool pp_chain, void* stream, int tmode = 0) {
     if (!pl || !tab || !Q || !work) return fail("null argument");
     const long long fs5 = 5 * pl->g.fs;
     double* Q1 = work;
@@ -2323,10 +2370,13 @@ static int stage_impl(hevi_plan* pl, int stage, double dt, const double* tab, do
     EArgs a = base_eargs(pl);
     a.dt = dt;
     a.stage = stage;
+    a.tmode = tmode;
     int mode;
     if (stage == 0) {
         mode = M_S1;
         pl->pp_ok[0] = pl->pp_ok[1] = 0;   // a new step: the solves will refill the P' planes
+        // split stage (tmode != 0) without the chain: both calls form P'(Q) over
+        // the window, the boundary call after the exchange refreshed the halos
         if (pl->eqset == 0 && pl->use_v2) {
             // P'(Q) into Q1 field 0: not written by stage 0 (it writes Q1 u, v),
             // overwritten by the stage-0 solve afterwards; with pp_chain the
@@ -2381,7 +2431,19 @@ int hevi_stage(hevi_plan* pl, int stage, double dt, const double* tab, double* Q
 int hevi_stage_ex(hevi_plan* pl, int stage, double dt, const double* tab, double* Q, double* work,
                   unsigned flags, void* stream) {
     const bool chain = stage == 0 && (flags & HEVI_STEP_PP_VALID) && pl && pp_chainable(pl);
-    return stage_impl(pl, stage, dt, tab, Q, work, chain, stream);
+    if ((flags & HEVI_STAGE_INTERIOR) && (flags & HEVI_STAGE_BOUNDARY))
+        return fail("HEVI_STAGE_INTERIOR and HEVI_STAGE_BOUNDARY are exclusive");
+    const int tmode = (flags & HEVI_STAGE_INTERIOR) ? 1 : (flags & HEVI_STAGE_BOUNDARY) ? 2 : 0;
+    return stage_impl(pl, stage, dt, tab, Q, work, chain, stream, tmode);
+}
+
+int hevi_stage_tiles(const hevi_plan* pl, int* n_interior, int* n_boundary) {
+    if (!pl || !n_interior || !n_boundary) return fail("null argument");
+    int tb[6];
+    tile_split(pl->g, 4, 4, tb);
+    *n_interior = (tb[3] - tb[2]) * (tb[5] - tb[4]);
+    *n_boundary = tb[0] * tb[1] - *n_interior;
+    return HEVI_OK;
 }
 
 int hevi_stage_solve(hevi_plan* pl, int stage, double lam, double* work, void* stream) {

@@ -231,25 +231,54 @@ class DistributedStepper:
             return [state]
         return [state, W[3][s:s + 1]]
 
-    def step_stages(self):
-        """Generator over the 8 ordered sub-steps (3 exchanges, 3 explicit
-        stages, 2 solves) so a single-process driver can interleave ranks."""
+    def step_stages(self, overlap=False):
+        """Generator over the ordered sub-steps (per stage: [the interior
+        tiles,] the halo exchange of the stage inputs, the stage [boundary
+        tiles], the solve) so a single-process driver can interleave ranks.
+        With ``overlap`` the interior tiles, which read no halo point a
+        neighbour provides, are evaluated before the exchange ("pre" marks
+        the point where they start)."""
         p, Q, W = self.plan, self.Q, self.work
-        yield ("exchange", self.stage_inputs(0))
-        p.stage(0, self.dt, self.tab, Q, W, pp_valid=self.chain)
-        p.stage_solve(0, self.lam, W)
-        yield ("exchange", self.stage_inputs(1))
-        p.stage(1, self.dt, self.tab, Q, W)
-        p.stage_solve(1, self.lam, W)
-        yield ("exchange", self.stage_inputs(2))
-        p.stage(2, self.dt, self.tab, Q, W)
+        for s in range(3):
+            pp = self.chain if s == 0 else False
+            if overlap:
+                yield ("pre", s)
+                p.stage(s, self.dt, self.tab, Q, W, pp_valid=pp, part="interior")
+            yield ("exchange", self.stage_inputs(s))
+            p.stage(s, self.dt, self.tab, Q, W, pp_valid=pp, part="boundary" if overlap else None)
+            if s < 2:
+                p.stage_solve(s, self.lam, W)
         yield ("done", None)
 
-    def step(self):
-        for kind, ts in self.step_stages():
-            if kind == "exchange":
-                for t in ts:
+    def step(self, side_stream=None):
+        """One step.  With a side CUDA stream the halo exchange of every stage
+        runs on it while the interior tiles run on the current stream; the
+        boundary tiles wait for the exchange (event), so the exchange latency
+        hides behind the interior sweep."""
+        if side_stream is None:
+            for kind, ts in self.step_stages():
+                if kind == "exchange":
+                    for t in ts:
+                        self.exchange(t)
+            return
+        import torch
+        main = torch.cuda.current_stream()
+        p, Q, W = self.plan, self.Q, self.work
+        for s in range(3):
+            pp = self.chain if s == 0 else False
+            ready = torch.cuda.Event()
+            ready.record(main)                    # the previous solve wrote the inputs
+            with torch.cuda.stream(side_stream):
+                side_stream.wait_event(ready)
+                for t in self.stage_inputs(s):
                     self.exchange(t)
+                done = torch.cuda.Event()
+                done.record(side_stream)
+            p.stage(s, self.dt, self.tab, Q, W, pp_valid=pp, part="interior")
+            main.wait_event(done)
+            p.stage(s, self.dt, self.tab, Q, W, pp_valid=pp, part="boundary")
+            if s < 2:
+                p.stage_solve(s, self.lam, W)
 
 
 class LocalExchange:
@@ -286,17 +315,24 @@ class LocalExchange:
                 self.fill(r, t_by_rank, phases=(ip,))
 
 
-def run_local_partitioned(steppers, exchange: LocalExchange, nsteps=1):
-    """Advance all emulated ranks in lock-step on one device."""
+def run_local_partitioned(steppers, exchange: LocalExchange, nsteps=1, overlap=False, pre=None):
+    """Advance all emulated ranks in lock-step on one device.  ``overlap``:
+    interior tiles before the exchange; ``pre(stepper, stage)`` runs on every
+    rank just before its interior tiles (tests poison the halos there)."""
     if exchange.plans is None:
         exchange.plans = [s.plan for s in steppers]
     for _ in range(nsteps):
-        gens = [s.step_stages() for s in steppers]
+        gens = [s.step_stages(overlap=overlap) for s in steppers]
         while True:
             items = [next(g) for g in gens]
             kind = items[0][0]
             if kind == "done":
                 break
+            if kind == "pre":
+                if pre is not None:
+                    for s, it in zip(steppers, items):
+                        pre(s, it[1])
+                continue
             lists = [it[1] for it in items]
             for j in range(len(lists[0])):
                 exchange.fill_all([lst[j] for lst in lists])

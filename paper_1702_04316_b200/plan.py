@@ -183,9 +183,25 @@ class HeviPlan:
     def rk35(self, dt, Q, work):
         nv.check(self.lib.hevi_rk35_step(self.h, float(dt), nv.ptr(Q), nv.ptr(work), nv.stream_ptr()))
 
-    def stage(self, s, dt, tab: np.ndarray, Q, work, pp_valid=False):
+    def stage(self, s, dt, tab: np.ndarray, Q, work, pp_valid=False, part=None):
+        """One explicit stage; ``part`` = "interior" | "boundary" evaluates the
+        tiles that read no neighbour-provided halo point (before the halo
+        exchange) or the rest (after it); None: the whole stage."""
+        flags = nv.STEP_PP_VALID if pp_valid else 0
+        if part == "interior":
+            flags |= nv.STAGE_INTERIOR
+        elif part == "boundary":
+            flags |= nv.STAGE_BOUNDARY
+        elif part is not None:
+            raise ValueError(f"unknown stage part {part!r}")
         nv.check(self.lib.hevi_stage_ex(self.h, s, float(dt), _dp(tab), nv.ptr(Q), nv.ptr(work),
-                                        nv.STEP_PP_VALID if pp_valid else 0, nv.stream_ptr()))
+                                        flags, nv.stream_ptr()))
+
+    def stage_tiles(self):
+        """(interior, boundary) tile counts of the column-sweep stage kernels."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        nv.check(self.lib.hevi_stage_tiles(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def stage_solve(self, s, lam, work):
         nv.check(self.lib.hevi_stage_solve(self.h, s, float(lam), nv.ptr(work), nv.stream_ptr()))
