@@ -1320,6 +1320,20 @@ namespace {
 
 long long lam_key(double lam) { return llround(lam * 1e12); }
 
+// dynamic shared-memory opt-in of a kernel, per device (the attribute is
+// per device: a process may drive several GPUs)
+template <typename K>
+int set_smem_attr(K kern, size_t smem, size_t (&done)[16]) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 16) return fail("device index out of range");
+    if (done[dev] < smem) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        done[dev] = smem;
+    }
+    return HEVI_OK;
+}
+
 // ---- explicit-kernel dispatch -------------------------------------------
 template <int NX, int NY>
 struct TileCfg;
@@ -1346,11 +1360,9 @@ int launch_e(const hevi_plan* pl, EArgs a, cudaStream_t st) {
     constexpr int TX = TileCfg<NX, NY>::TX, TY = TileCfg<NX, NY>::TY;
     using T = ETile<NX, NY, NX, TX, TY>;
     auto kern = k_explicit<NX, NY, NX, TX, TY, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
-        attr = true;
-    }
+    static size_t attr[16] = {0};
+    int rc = set_smem_attr(kern, T::SMEM, attr);
+    if (rc) return rc;
     const Geo& g = pl->g;
     dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
     kern<<<grid, T::BLK, T::SMEM, st>>>(a);
@@ -1452,13 +1464,11 @@ int launch_e2(const hevi_plan* pl, const EArgs& a, cudaStream_t st, bool& done) 
         const size_t smem = T::fixed_bytes(MODE) + sizeof(double) * T::NTAB * g.Z;
         if (smem > 225 * 1024) return HEVI_OK;   // v1 handles it
         auto kern = k_explicit2<N, NY, TX, TY, MODE, Tile2<N, NY>::MINB>;
-        static size_t attr = 0;
-        if (attr < smem) {
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = smem;
-        }
+        static size_t attr[16] = {0};
+        int rc = set_smem_attr(kern, smem, attr);
+        if (rc) return rc;
         CUtensorMap tm;
-        int rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, 1);   // one level per TMA
+        rc = make_tmap(&tm, g, a.q, T::LXT, T::LY, 1);   // one level per TMA
         if (rc) return rc;
         EArgs a2 = a;
         a2.af_tma = 0;
@@ -1555,11 +1565,9 @@ int launch_c(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     } else {
         using T = ECT<N, NY, TX, TY>;
         auto kern = k_explicit_c<N, NY, TX, TY, MODE>;
-        static bool attr = false;
-        if (!attr) {
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
-            attr = true;
-        }
+        static size_t attr[16] = {0};
+        int rc = set_smem_attr(kern, T::SMEM, attr);
+        if (rc) return rc;
         const Geo& g = pl->g;
         dim3 grid((g.ex_e - g.ex_b + TX - 1) / TX, (g.ey_e - g.ey_b + TY - 1) / TY);
         kern<<<grid, T::BLK, T::SMEM, st>>>(a);
@@ -1596,17 +1604,6 @@ int dispatch_c(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
 
 // ---- explicit_col dispatch (3D box, N = 4, set2nc, stage kernels) --------
 // cudaFuncSetAttribute once per (kernel, device)
-template <typename K>
-int set_smem_attr(K kern, size_t smem, size_t (&done)[16]) {
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 16) return fail("device index out of range");
-    if (done[dev] < smem) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        done[dev] = smem;
-    }
-    return HEVI_OK;
-}
 
 bool col_applies(const hevi_plan* pl, int mode, const EArgs& a) {
     const Geo& g = pl->g;
@@ -1849,12 +1846,9 @@ int launch_s(const hevi_plan* pl, SArgs a, cudaStream_t st) {
     while (T > 32 && fixed + sizeof(double) * 2 * (size_t)M * T > 200 * 1024) T /= 2;
     const size_t smem = fixed + sizeof(double) * 2 * (size_t)M * T;
     if (smem > 227 * 1024) return fail("column too tall for the shared-memory column kernel");
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(k_solve<NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024));
-        attr = true;
-    }
+    static size_t attr[16] = {0};
+    int rc = set_smem_attr(k_solve<NZ>, 227 * 1024, attr);
+    if (rc) return rc;
     const int NYo = g.slab ? 1 : pl->N;
     const long long cntx = (long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0);
     const long long cnty = (long long)(g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
@@ -1908,23 +1902,16 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
     }
     const size_t smem = s2_smem_bytes<N>(M, T);
     if (smem > 225 * 1024) return fail("column too tall for the v2 column kernel");
-    static size_t attr = 0;
-    if (attr < smem) {
-        CK(cudaFuncSetAttribute(k_solve2<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-        attr = smem;
-    }
+    static size_t attr[16] = {0};
+    int rc = set_smem_attr(k_solve2<N, false>, smem, attr);
+    if (rc) return rc;
     const int NYo = g.slab ? 1 : pl->N;
     const long long cntx = (long long)(g.ex_e - g.ex_b) * pl->N + (g.ex_e == g.nex ? 1 : 0);
     const long long cnty = (long long)(g.ey_e - g.ey_b) * NYo + (g.ey_e == g.ney ? 1 : 0);
     const int nblk = (int)((cntx * cnty + T - 1) / T);
     if (pl->eqset == 1) {
-        static size_t attrc = 0;
-        if (attrc < smem) {
-            CK(cudaFuncSetAttribute(k_solve2<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-            attrc = smem;
-        }
+        static size_t attrc[16] = {0};
+        if ((rc = set_smem_attr(k_solve2<N, true>, smem, attrc))) return rc;
     }
     auto kern = pl->eqset == 1 ? k_solve2<N, true> : k_solve2<N, false>;
     // persistent grid: every resident CTA slot once (the records load once per CTA)
