@@ -4,8 +4,9 @@ case).  Run in the build container, where /root/reference exists:
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_sphere_golden.py
 
-Case ``sphere_n4`` (and ``sphere_n3``): build_cubed_sphere_mesh(ne_panel=2,
-ne_vert=2, r_e, r_T = the AcousticWaveConfig shell, N), the isothermal 300 K
+Cases ``sphere_n3``, ``sphere_n4`` (ne_panel = ne_vert = 2) and ``sphere_n8``
+(ne_panel = ne_vert = 1, the largest element the device kernels take):
+build_cubed_sphere_mesh(ne_panel, ne_vert, r_e, r_T = the AcousticWaveConfig shell, N), the isothermal 300 K
 background the reference driver uses for the acoustic case (cli.py:131-141),
 the balanced acoustic pulse (bench.init_acoustic_wave) plus a DSS-projected
 random velocity, and through the reference's public API:
@@ -78,8 +79,8 @@ def run_case(N, ne_panel=2, ne_vert=2, seed=7):
 
 
 def main():
-    for N in (3, 4):
-        out = run_case(N)
+    for N, ne_p, ne_v in ((3, 2, 2), (4, 2, 2), (8, 1, 1)):
+        out = run_case(N, ne_p, ne_v)
         path = os.path.join(HERE, f"sphere_n{N}.npz")
         np.savez_compressed(path, **out)
         print(path, os.path.getsize(path))
