@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
         double* pb = PB + (l & 1) * T::PBS;
         const double rho0 = lt.v[C_RHO0][l], Th0 = lt.v[C_TH0C][l];
         const PPc ppc = ecc_ppc(a, lt, l);
-#pragma unroll 1
+        static_assert(LY * LXT <= 2 * BLK, "convert: two passes over the staged plane");
+#pragma unroll
         for (int i = tid; i < LY * LXT; i += BLK) {
             const double r = slot[i], U = slot[PL + i], V = slot[2 * PL + i], W = slot[3 * PL + i],
                          Th = slot[4 * PL + i];
@@ -235,7 +236,8 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
         const double* pb = PB + (l & 1) * T::PBS;
         double* xf = XFb + buf * T::NXF;
         double* yf = YFb + buf * T::NYF;
-#pragma unroll 1
+        static_assert(T::NXF + T::NYF <= 3 * BLK, "faces: three passes");
+#pragma unroll
         for (int i = tid; i < T::NXF + T::NYF; i += BLK) {
             if (i < T::NXF) {
                 const int q = i / (OY * TX), rem = i % (OY * TX);
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
     __syncthreads();
 
     int k = 0;
+    unsigned fl = 0;
     for (int l = 0; l < Z; ++l) {
         const bool top = (l == Z - 1);
         if (k == 0 && !top) {
@@ -343,14 +346,15 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
             for (int m = 1; m <= N; ++m) dz = fma(dzr[m], Wz[f][m], dz);
             gzq[f] = fma(czf, car[f], dz);
         }
-        if (own) {
+        {
+            // every thread computes; only owned points store or raise flags
+            // (branch-free bits, one atomic per thread at the end)
             const double rho = lt.v[C_RHO0][l] + r;
             const double Theta = lt.v[C_TH0C][l] + Th;
-            if (!isfinite(((r + U) + (V + W)) + Th)) {
-                if (!(isfinite(r) && isfinite(U) && isfinite(V) && isfinite(W) && isfinite(Th)))
-                    atomicOr(a.flags, HEVI_F_NONFINITE_IN(a.stage));
-            }
-            if (!(rho > 0.0) || !(Theta / rho > 0.0)) atomicOr(a.flags, HEVI_F_EOS(a.stage));
+            const double zc = fma(r, 0.0, fma(U, 0.0, fma(V, 0.0, fma(W, 0.0, Th * 0.0))));
+            unsigned b = (zc == zc) ? 0u : HEVI_F_NONFINITE_IN(a.stage);
+            b |= (rho > 0.0 && Theta / rho > 0.0) ? 0u : HEVI_F_EOS(a.stage);
+            fl |= own ? b : 0u;
             double Ai[5] = {0, 0, 0, 0, 0}, Fi[5] = {0, 0, 0, 0, 0};
             if (T::NAF) {
                 mbar_wait(&mbar[S + l % T::SAFM], (l / T::SAFM) & 1);
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
             p.v = V;
             p.w = W;
             p.th = Th;
-            ec_epilogue<MODE>(a, lt, colo + (long long)l * zs, l, p, Rv, Lv, Ai, Fi, bx, by);
+            ec_epilogue<MODE>(a, lt, colo + (long long)l * zs, l, p, Rv, Lv, Ai, Fi, bx, by, own, &fl);
         }
         if (l + 1 < Z) convert(l + 1);
         __syncthreads();
@@ -387,6 +391,7 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
         }
         if (!top) k = (k + 1 == N) ? 0 : k + 1;
     }
+    if (fl) atomicOr(a.flags, fl);
 }
 
 // set2c domain-end planes: one thread per point, the quantities formed per
