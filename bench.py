@@ -386,16 +386,16 @@ def run_gpu(args):
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     halo0 = ds.exchange.launches if world > 1 else 0
+    # the timed steps: nothing recorded between the launches
     t_start.record(stream)
     for k in range(args.steps):
-        one_step(evs[k])
+        one_step()
     t_end.record(stream)
     torch.cuda.synchronize()
     halo_launches = (ds.exchange.launches - halo0) if world > 1 else 0
@@ -403,6 +403,17 @@ def run_gpu(args):
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     elapsed = t_start.elapsed_time(t_end)    # ms
+    # per-launch times: the same steps again with CUDA events around every
+    # launch on the launching stream (their shares scale the timed total)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    i_start = torch.cuda.Event(enable_timing=True)
+    i_end = torch.cuda.Event(enable_timing=True)
+    i_start.record(stream)
+    for k in range(args.steps):
+        one_step(evs[k])
+    i_end.record(stream)
+    torch.cuda.synchronize()
+    instr_elapsed = i_start.elapsed_time(i_end)
     ktimes = {n: 0.0 for n in names}
     for ev in ([] if rk else evs):
         ktimes["explicit_stage0"] += ev[0].elapsed_time(ev[1])
@@ -431,7 +442,7 @@ def run_gpu(args):
             continue
         gbs = kb[n] * pts_rank / (avg * 1e-3) / 1e9
         kern[n] = {"ms": round(avg, 4), "alg_bytes_per_point": kb[n],
-                   "alg_GBps": round(gbs, 1), "share": round(ktimes[n] / elapsed, 4)}
+                   "alg_GBps": round(gbs, 1), "share": round(ktimes[n] / instr_elapsed, 4)}
     if rk:   # whole RK35 step: 5 fused R + Shu-Osher launches (13 reads + 5 writes per point)
         kern = {"rk35_step": {"ms": round(ms_step, 4), "alg_bytes_per_point": 8 * 5 * 18,
                               "alg_GBps": round(8 * 5 * 18 * pts_rank / (ms_step * 1e-3) / 1e9, 1),
@@ -498,6 +509,7 @@ def run_gpu(args):
                                 % (8 * dof / 1e6)},
                "storage_dof_per_s": 5 * mesh.n_nodes / (ms_step * 1e-3),
                "roofline": roof, "step_roofline": step_roof, "kernels": kern,
+               "kernels_pass_ms_per_step": round(instr_elapsed / args.steps, 4),
                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
                "setup": {"factor_ms": round(factor_ms, 3),
                          "what": "columnsolve.get_factors on the device (k_lamtab + k_probe + "
