@@ -14,6 +14,7 @@ def main():
     from paper_1702_04316_b200 import specgrid, euler, imexcore, cases
     from paper_1702_04316_b200.plan import tableau_array
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+    graph = "graph" in sys.argv[2:]
     mesh = specgrid.build_box_mesh_3d(176, 176, 10, 704_000.0, 704_000.0, 1000.0, 4)
     ref = euler.hydrostatic_reference(mesh, 300.0)
     disc = euler.build_discretization(mesh)
@@ -29,18 +30,27 @@ def main():
     for _ in range(5):
         p.step(dt, tarr, Q, W, pp_valid=True)
     p.check_flags()
+    g = None
+    if graph:   # one step captured as a CUDA graph, replayed
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            p.step(dt, tarr, Q, W, pp_valid=True)
     out = []
     for rep in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
         for _ in range(steps):
-            p.step(dt, tarr, Q, W, pp_valid=True)
+            if g is not None:
+                g.replay()
+            else:
+                p.step(dt, tarr, Q, W, pp_valid=True)
         e1.record()
         torch.cuda.synchronize()
         out.append(e0.elapsed_time(e1) / steps)
     p.check_flags()
-    print(os.environ.get("HEVI_LIB", "libhevi.so"), " ".join(f"{v:.4f}" for v in out), "ms/step")
+    print(os.environ.get("HEVI_LIB", "libhevi.so"), "graph" if graph else "eager", " ".join(f"{v:.4f}" for v in out), "ms/step")
 
 
 if __name__ == "__main__":
