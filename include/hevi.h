@@ -309,6 +309,18 @@ int hevi_g_dss(hevi_gplan *plan, const double *in, double *out, int nf, void *st
 int hevi_g_grad(hevi_gplan *plan, int vertical_only, const double *f, double *out, void *stream);
 int hevi_g_div(hevi_gplan *plan, int vertical_only, const double *vec, double *out, void *stream);
 int hevi_g_flags(hevi_gplan *plan, unsigned *flags, int reset, void *stream);
+/* 3D-IMEX on the general mesh (ImplicitProblem dim "3d", or "1d" with
+ * vertical_only): the Schur pieces of imexcore.py:200-298 on E-vectors,
+ * euler.linear_operator (euler.py:313-365), and the Krylov solvers' plain
+ * dot product over n doubles (krylov.py:46-55) */
+int hevi_g_schur3_ua(hevi_gplan *plan, double lam, const double *qe, double *ua, double *Pe, void *stream);
+int hevi_g_schur3_up(hevi_gplan *plan, double lam, int vertical_only, const double *P, double *up, void *stream);
+int hevi_g_schur3_flux(hevi_gplan *plan, double lam, int vertical_only, const double *P, const double *vel,
+                       double *out, void *stream);
+int hevi_g_schur3_extract(hevi_gplan *plan, double lam, int vertical_only, const double *P, const double *ua,
+                          const double *up, const double *qe, double *q, void *stream);
+int hevi_g_linear3(hevi_gplan *plan, const double *q, double *out, void *stream);
+int hevi_g_dot(hevi_gplan *plan, const double *x, const double *y, long long n, double *out_host, void *stream);
 
 #ifdef __cplusplus
 }

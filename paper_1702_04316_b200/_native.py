@@ -130,6 +130,12 @@ SIGNATURES = {
     "hevi_g_grad": (_I, [_V, _I, _V, _V, _V]),
     "hevi_g_div": (_I, [_V, _I, _V, _V, _V]),
     "hevi_g_flags": (_I, [_V, ctypes.POINTER(ctypes.c_uint), _I, _V]),
+    "hevi_g_schur3_ua": (_I, [_V, _D, _V, _V, _V, _V]),
+    "hevi_g_schur3_up": (_I, [_V, _D, _I, _V, _V, _V]),
+    "hevi_g_schur3_flux": (_I, [_V, _D, _I, _V, _V, _V, _V]),
+    "hevi_g_schur3_extract": (_I, [_V, _D, _I, _V, _V, _V, _V, _V, _V]),
+    "hevi_g_linear3": (_I, [_V, _V, _V, _V]),
+    "hevi_g_dot": (_I, [_V, _V, _V, _LL, ctypes.POINTER(_D), _V]),
 }
 
 _lib = None

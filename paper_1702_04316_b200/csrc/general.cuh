@@ -594,3 +594,161 @@ __global__ void kg_times_vert(const GGeo g, const double* __restrict__ d, double
         out[2 * nn + n] = v * g.vert[2 * nn + n];
     }
 }
+
+// ---------------------------------------------------------------------------
+// 3D-IMEX pieces on the general mesh (ImplicitProblem dim = "3d",
+// imexcore.py:200-298 with gradc / divc): pointwise parts; the DSS-projected
+// gradient / divergence come from kg_graddiv + kg_dss
+// ---------------------------------------------------------------------------
+// A^-1 v (imexcore._ainv, :200-216) and the no-flux projection of the node
+__device__ __forceinline__ void g_ainv_proj(const GGeo& g, const GRef& r, long long n, double lam, double& x,
+                                            double& y, double& z, unsigned* flags) {
+    const long long nn = g.nn;
+    if (!r.w_zero) {
+        const double sc = (lam * lam) / r.theta0[n];
+        const double u0 = sc * r.gvec[n], u1 = sc * r.gvec[nn + n], u2 = sc * r.gvec[2 * nn + n];
+        const double den = 1.0 + dot3(r.gth0, nn, n, u0, u1, u2);
+        if (fabs(den) < 1e-12) atomicOr(flags, HEVI_F_AINV);
+        const double wv = dot3(r.gth0, nn, n, x, y, z) / den;
+        x = x - u0 * wv;
+        y = y - u1 * wv;
+        z = z - u2 * wv;
+    }
+    g_project(g, g.bslot[n], x, y, z);
+}
+
+// rhs_schur_build's ua and Pe (imexcore.py:229-243): ua -> [3][nn], Pe -> [nn]
+__global__ void kg_schur_ua(const GGeo g, const GRef r, const double* __restrict__ qe, double lam,
+                            double* __restrict__ ua, double* __restrict__ Pe, unsigned* flags) {
+    const long long nn = g.nn;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nn; n += (long long)gridDim.x * blockDim.x) {
+        double x, y, z;
+        if (r.eqset == 0) {
+            const double s = ((lam * r.H0[n]) / (r.G0[n] * r.rho0[n])) * qe[4 * nn + n];
+            x = qe[nn + n] + s * r.gvec[n];
+            y = qe[2 * nn + n] + s * r.gvec[nn + n];
+            z = qe[3 * nn + n] + s * r.gvec[2 * nn + n];
+            Pe[n] = r.G0[n] * qe[n] + r.H0[n] * qe[4 * nn + n];
+        } else {
+            const double s = lam * (qe[n] - qe[4 * nn + n] / r.theta0[n]);
+            x = qe[nn + n] - s * r.gvec[n];
+            y = qe[2 * nn + n] - s * r.gvec[nn + n];
+            z = qe[3 * nn + n] - s * r.gvec[2 * nn + n];
+            Pe[n] = r.F0c[n] * qe[4 * nn + n];
+        }
+        g_ainv_proj(g, r, n, lam, x, y, z, flags);
+        ua[n] = x;
+        ua[nn + n] = y;
+        ua[2 * nn + n] = z;
+    }
+}
+
+// _up(P) from the DSS-projected gradient gP [3][nn] (imexcore.py:245-257)
+__global__ void kg_up3(const GGeo g, const GRef r, const double* __restrict__ P, const double* __restrict__ gP,
+                       double lam, double* __restrict__ up, unsigned* flags) {
+    const long long nn = g.nn;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nn; n += (long long)gridDim.x * blockDim.x) {
+        double x, y, z;
+        if (r.eqset == 0) {
+            const double rr = r.rho0[n], s = P[n] / (r.G0[n] * rr);
+            x = lam * (gP[n] / rr + s * r.gvec[n]);
+            y = lam * (gP[nn + n] / rr + s * r.gvec[nn + n]);
+            z = lam * (gP[2 * nn + n] / rr + s * r.gvec[2 * nn + n]);
+        } else {
+            const double s = P[n] / (r.F0c[n] * r.theta0[n]);
+            x = lam * (gP[n] + s * r.gvec[n]);
+            y = lam * (gP[nn + n] + s * r.gvec[nn + n]);
+            z = lam * (gP[2 * nn + n] + s * r.gvec[2 * nn + n]);
+        }
+        g_ainv_proj(g, r, n, lam, x, y, z, flags);
+        up[n] = x;
+        up[nn + n] = y;
+        up[2 * nn + n] = z;
+    }
+}
+
+// extract_from_pressure (imexcore.py:273-298); vo: 1d (advection by the
+// vertical part of the velocity) or 3d (the whole velocity)
+__global__ void kg_extract3(const GGeo g, const GRef r, const double* __restrict__ P, const double* __restrict__ ua,
+                            const double* __restrict__ up, const double* __restrict__ qe, double lam, int vo,
+                            double* __restrict__ q) {
+    const long long nn = g.nn;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nn; n += (long long)gridDim.x * blockDim.x) {
+        const double w0 = ua[n] - up[n], w1 = ua[nn + n] - up[nn + n], w2 = ua[2 * nn + n] - up[2 * nn + n];
+        double a0 = w0, a1 = w1, a2 = w2;
+        if (vo) {
+            const double v0 = g.vert[n], v1 = g.vert[nn + n], v2 = g.vert[2 * nn + n];
+            const double uv = (w0 * v0 + w1 * v1) + w2 * v2;
+            a0 = uv * v0;
+            a1 = uv * v1;
+            a2 = uv * v2;
+        }
+        const double Pn = P[n];
+        double q0, q4;
+        if (r.eqset == 0) {
+            q4 = qe[4 * nn + n] - lam * dot3(r.gth0, nn, n, a0, a1, a2);
+            q0 = (Pn - r.H0[n] * q4) / r.G0[n];
+        } else {
+            const double G0 = r.theta0[n];
+            q4 = Pn / r.F0c[n];
+            q0 = ((Pn / (r.F0c[n] * G0) + lam / G0 * dot3(r.gth0, nn, n, a0, a1, a2)) - qe[4 * nn + n] / G0) + qe[n];
+        }
+        q[n] = q0;
+        q[nn + n] = w0;
+        q[2 * nn + n] = w1;
+        q[3 * nn + n] = w2;
+        q[4 * nn + n] = q4;
+    }
+}
+
+// the full 3D linear operator (euler.linear_operator, dim 3d, euler.py:313-365)
+// from gP = gradc(P_lin) [3][nn] and dV = divc(velocity) [nn]
+__global__ void kg_lin3(const GGeo g, const GRef r, const double* __restrict__ q, const double* __restrict__ gP,
+                        const double* __restrict__ dV, double* __restrict__ out) {
+    const long long nn = g.nn;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nn; n += (long long)gridDim.x * blockDim.x) {
+        const double u0 = q[nn + n], u1 = q[2 * nn + n], u2 = q[3 * nn + n], q0 = q[n];
+        double m0, m1, m2;
+        if (r.eqset == 0) {
+            out[n] = -(dot3(r.grho0, nn, n, u0, u1, u2) + r.rho0[n] * dV[n]);
+            const double rr = r.rho0[n], qr = q0 / rr;
+            m0 = -(gP[n] / rr + qr * r.gvec[n]);
+            m1 = -(gP[nn + n] / rr + qr * r.gvec[nn + n]);
+            m2 = -(gP[2 * nn + n] / rr + qr * r.gvec[2 * nn + n]);
+            out[4 * nn + n] = -dot3(r.gth0, nn, n, u0, u1, u2);
+        } else {
+            out[n] = -dV[n];
+            m0 = -(gP[n] + q0 * r.gvec[n]);
+            m1 = -(gP[nn + n] + q0 * r.gvec[nn + n]);
+            m2 = -(gP[2 * nn + n] + q0 * r.gvec[2 * nn + n]);
+            out[4 * nn + n] = -(r.theta0[n] * dV[n] + dot3(r.gth0, nn, n, u0, u1, u2));
+        }
+        g_project(g, g.bslot[n], m0, m1, m2);
+        out[nn + n] = m0;
+        out[2 * nn + n] = m1;
+        out[3 * nn + n] = m2;
+    }
+}
+
+// linearised pressure of the state (euler.py:188-194) -> [nn]
+__global__ void kg_plin(const GGeo g, const GRef r, const double* __restrict__ q, double* __restrict__ P) {
+    const long long nn = g.nn;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nn; n += (long long)gridDim.x * blockDim.x)
+        P[n] = r.eqset == 0 ? r.G0[n] * q[n] + r.H0[n] * q[4 * nn + n] : r.F0c[n] * q[4 * nn + n];
+}
+
+// plain dot product over n doubles in a fixed order (the reference's np.dot
+// over E-vectors, krylov.py:46-55): per-block partial sums, then one thread
+__global__ void kg_dot(const double* __restrict__ x, const double* __restrict__ y, long long n, double* part) {
+    __shared__ double sm[KV_T];
+    double s = 0.0;
+    for (long long i = (long long)blockIdx.x * KV_T + threadIdx.x; i < n; i += (long long)KV_BLOCKS * KV_T)
+        s = fma(x[i], y[i], s);
+    sm[threadIdx.x] = s;
+    __syncthreads();
+    for (int t = KV_T / 2; t > 0; t >>= 1) {
+        if (threadIdx.x < t) sm[threadIdx.x] += sm[threadIdx.x + t];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}

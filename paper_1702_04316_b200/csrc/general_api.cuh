@@ -329,3 +329,87 @@ int hevi_g_flags(hevi_gplan* gp, unsigned* flags, int reset, void* stream) {
     if (!gp || !flags) return fail("null argument");
     return g_flags_now(gp, flags, reset, (cudaStream_t)stream);
 }
+
+// ---- 3D-IMEX pieces (ImplicitProblem dim = "3d" / "1d" Krylov path) --------
+int hevi_g_schur3_ua(hevi_gplan* gp, double lam, const double* qe, double* ua, double* Pe, void* stream) {
+    if (!gp || !qe || !ua || !Pe) return fail("null argument");
+    kg_schur_ua<<<blocks_for(gp->nn), 256, 0, (cudaStream_t)stream>>>(gp->g, gp->r, qe, lam, ua, Pe, gp->d_flags);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_g_schur3_up(hevi_gplan* gp, double lam, int vertical_only, const double* P, double* up, void* stream) {
+    if (!gp || !P || !up) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    if (vertical_only) {
+        if ((rc = g_vgrad(gp, P, st))) return rc;
+        kg_up<<<blocks_for(gp->nn), 256, 0, st>>>(gp->g, gp->r, P, gp->s0, lam, up, gp->d_flags);
+    } else {
+        G_DISPATCH(gp->g.nq, { kg_graddiv<NQ><<<gp->g.nel, NQ * NQ * NQ, 0, st>>>(gp->g, P, 0, gp->up); });
+        CK(cudaGetLastError());
+        if ((rc = g_dss(gp, gp->up, gp->up, 3, 0, st))) return rc;
+        kg_up3<<<blocks_for(gp->nn), 256, 0, st>>>(gp->g, gp->r, P, gp->up, lam, up, gp->d_flags);
+    }
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_g_schur3_flux(hevi_gplan* gp, double lam, int vertical_only, const double* P, const double* vel,
+                       double* out, void* stream) {
+    if (!gp || !P || !vel || !out) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    if (vertical_only) {
+        GVArgs a = {};
+        a.vec = const_cast<double*>(vel);
+        a.d0 = gp->s1;
+        if ((rc = g_vderiv(gp, a, 3, st))) return rc;
+    } else {
+        G_DISPATCH(gp->g.nq, { kg_graddiv<NQ><<<gp->g.nel, NQ * NQ * NQ, 0, st>>>(gp->g, vel, 1, gp->s1); });
+        CK(cudaGetLastError());
+    }
+    if ((rc = g_dss(gp, gp->s1, gp->s1, 1, 0, st))) return rc;
+    kg_lhs<<<blocks_for(gp->nn), 256, 0, st>>>(gp->g, gp->r, P, vel, gp->s1, lam, out);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_g_schur3_extract(hevi_gplan* gp, double lam, int vertical_only, const double* P, const double* ua,
+                          const double* up, const double* qe, double* q, void* stream) {
+    if (!gp || !P || !ua || !up || !qe || !q) return fail("null argument");
+    kg_extract3<<<blocks_for(gp->nn), 256, 0, (cudaStream_t)stream>>>(gp->g, gp->r, P, ua, up, qe, lam,
+                                                                      vertical_only, q);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_g_linear3(hevi_gplan* gp, const double* q, double* out, void* stream) {
+    if (!gp || !q || !out) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    kg_plin<<<blocks_for(gp->nn), 256, 0, st>>>(gp->g, gp->r, q, gp->sP);
+    CK(cudaGetLastError());
+    G_DISPATCH(gp->g.nq, {
+        kg_graddiv<NQ><<<gp->g.nel, NQ * NQ * NQ, 0, st>>>(gp->g, gp->sP, 0, gp->up);
+        kg_graddiv<NQ><<<gp->g.nel, NQ * NQ * NQ, 0, st>>>(gp->g, q + gp->nn, 1, gp->s1);
+    });
+    CK(cudaGetLastError());
+    int rc;
+    if ((rc = g_dss(gp, gp->up, gp->up, 3, 0, st)) || (rc = g_dss(gp, gp->s1, gp->s1, 1, 0, st))) return rc;
+    kg_lin3<<<blocks_for(gp->nn), 256, 0, st>>>(gp->g, gp->r, q, gp->up, gp->s1, out);
+    CK(cudaGetLastError());
+    return HEVI_OK;
+}
+
+int hevi_g_dot(hevi_gplan* gp, const double* x, const double* y, long long n, double* out_host, void* stream) {
+    if (!gp || !x || !y || !out_host) return fail("null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    double* part = gp->sO;   // KV_BLOCKS partials (scratch) and the sum after them
+    if (gp->nn < KV_BLOCKS + 1) return fail("general plan too small for the dot scratch");
+    kg_dot<<<KV_BLOCKS, KV_T, 0, st>>>(x, y, n, part);
+    k3_sum<<<1, 32, 0, st>>>(part, KV_BLOCKS, part + KV_BLOCKS);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_host, part + KV_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return HEVI_OK;
+}

@@ -122,9 +122,6 @@ def parse_config(path=None, overrides=()) -> RunConfig:
 
 
 def _check_supported(cfg: RunConfig):
-    if cfg.case == "acoustic" and cfg.integrator in ("ark2", "bdf2") and cfg.solver != "direct":
-        raise NotImplementedError("on the cubed-sphere shell the device path runs the 1D-IMEX "
-                                  "direct solve (imex=1d, solver=direct) and RK35")
     if cfg.disc != "cg":
         raise NotImplementedError("dG is outside the HEVI direct path")
     if cfg.integrator in ("ark2", "bdf2") and cfg.form != "schur":
@@ -485,12 +482,15 @@ def _run_sphere(cfg: RunConfig, quiet=False) -> RunResult:
             elif cfg.integrator == "ark2" or q_prev is None or step_dt != dt:
                 if cfg.integrator == "bdf2":
                     q_prev = Q.clone()
-                problem.lam = ark.diag * step_dt
-                inplace = True
-                plan.step(step_dt, tarr, Q, work)
-                plan.check_flags()
-                inplace = False
-                problem.stats.solves += 2
+                if problem.fused:       # 1D-IMEX direct: the device step
+                    problem.lam = ark.diag * step_dt
+                    inplace = True
+                    plan.step(step_dt, tarr, Q, work)
+                    plan.check_flags()
+                    inplace = False
+                    problem.stats.solves += 2
+                else:                   # Krylov solves: the reference stage loop on the device operators
+                    Q.copy_(imexcore.ark_imex_step(Q.clone(), step_dt, ark, problem, rhs))
             else:
                 qn = Q.clone()
                 Q.copy_(imexcore.bdf2_imex_step(qn, q_prev, step_dt, bdf, problem, rhs))

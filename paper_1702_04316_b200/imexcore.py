@@ -355,13 +355,13 @@ class ImplicitProblem:
             return plan.schur3_flux(lam, v, up, plan.zeros(1)[0], vo)
 
         amap = krylov.LinearMap(int(np.prod(self.disc.mesh.nshape)), lhs_schur,
-                                space=krylov.LatticeSpace(plan))
+                                space=krylov.space_for(plan))
         x, rep = self._run_krylov(amap, rhs, Pe)
         self.stats.add(rep)
         if not rep.converged:
             raise SolverFailure(rep)
         plan.schur3_up(lam, x, up, vo)
-        q = plan.schur3_extract(lam, x, ua, up, Qe, plan.zeros())
+        q = plan.schur3_extract(lam, x, ua, up, Qe, plan.zeros(), vertical_only=vo)
         return back(plan.l2e(q))
 
     def _solve_standard(self, plan, Qe, lam):

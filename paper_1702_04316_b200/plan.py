@@ -225,7 +225,9 @@ class HeviPlan:
         nv.check(self.lib.hevi_schur3_ua(self.h, float(lam), nv.ptr(qe), nv.ptr(ua), nv.ptr(Pe),
                                          nv.stream_ptr()))
 
-    def schur3_extract(self, lam, P, ua, up, qe, q):
+    def schur3_extract(self, lam, P, ua, up, qe, q, vertical_only=False):
+        # the box's grad theta0 is vertical: advecting by the vertical part of
+        # the velocity or by all of it is the same product (imexcore.py:280-297)
         nv.check(self.lib.hevi_schur3_extract(self.h, float(lam), nv.ptr(P), nv.ptr(ua), nv.ptr(up),
                                               nv.ptr(qe), nv.ptr(q), nv.stream_ptr()))
         return q

@@ -629,6 +629,62 @@ class GPlan:
         nv.check(self.lib.hevi_g_div(self.h, int(bool(vertical_only)), nv.ptr(v), nv.ptr(out), self._s()))
         return out
 
+    # -- the Krylov (3D-IMEX) path: the box plan's names, on E-vectors -----------
+    def e2l(self, E, out=None, nf=None):
+        """This path keeps E-vectors: identity (the box plan converts to its lattice)."""
+        if out is None:
+            return E.contiguous()
+        out.copy_(E)
+        return out
+
+    def l2e(self, L, out=None):
+        if out is None:
+            return L
+        out.copy_(L)
+        return out
+
+    def krylov_space(self, nf=1):
+        from . import krylov
+        return krylov.EvecSpace(self)
+
+    def schur3_ua(self, lam, qe, ua, Pe):
+        from . import _native as nv
+        nv.check(self.lib.hevi_g_schur3_ua(self.h, float(lam), nv.ptr(qe), nv.ptr(ua), nv.ptr(Pe), self._s()))
+
+    def schur3_up(self, lam, P, up, vertical_only=False):
+        from . import _native as nv
+        nv.check(self.lib.hevi_g_schur3_up(self.h, float(lam), int(vertical_only), nv.ptr(P), nv.ptr(up),
+                                           self._s()))
+        return up
+
+    def schur3_flux(self, lam, P, vel, out, vertical_only=False):
+        from . import _native as nv
+        nv.check(self.lib.hevi_g_schur3_flux(self.h, float(lam), int(vertical_only), nv.ptr(P), nv.ptr(vel),
+                                             nv.ptr(out), self._s()))
+        return out
+
+    def schur3_extract(self, lam, P, ua, up, qe, q, vertical_only=False):
+        from . import _native as nv
+        nv.check(self.lib.hevi_g_schur3_extract(self.h, float(lam), int(vertical_only), nv.ptr(P), nv.ptr(ua),
+                                                nv.ptr(up), nv.ptr(qe), nv.ptr(q), self._s()))
+        return q
+
+    def linear3(self, q, out):
+        from . import _native as nv
+        nv.check(self.lib.hevi_g_linear3(self.h, nv.ptr(q), nv.ptr(out), self._s()))
+        return out
+
+    def wdot(self, x, y, nf=1) -> float:
+        from . import _native as nv
+        out = ctypes.c_double()
+        nv.check(self.lib.hevi_g_dot(self.h, nv.ptr(x), nv.ptr(y), x.numel(), ctypes.byref(out), self._s()))
+        return out.value
+
+    def axpby(self, alpha, x, beta, y):
+        from . import _native as nv
+        nv.check(self.lib.hevi_axpby(y.numel(), float(alpha), nv.ptr(x), float(beta), nv.ptr(y), self._s()))
+        return y
+
     def flags(self, reset=True) -> int:
         from . import _native as nv
         f = ctypes.c_uint()
@@ -650,6 +706,8 @@ class GPlan:
             self.rhs(E, out)
         elif op == "linear":
             self.linear(E, out)
+        elif op == "linear3":
+            self.linear3(E, out)
         elif op == "solve":
             self.solve(lam, E, out)
         else:

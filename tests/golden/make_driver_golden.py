@@ -39,6 +39,9 @@ CASES = {
                       "--ne_panel=2", "--ne_vert=2", "--order=3", "--courant=4", "--end_time=60"],
     "acoustic_rk35": ["--case=acoustic", "--integrator=rk35", "--ne_panel=2", "--ne_vert=1",
                       "--order=3", "--courant=0.5", "--end_time=4"],
+    "acoustic_ark2_3d": ["--case=acoustic", "--integrator=ark2", "--imex=3d", "--solver=gmres",
+                         "--tolerance=1e-10", "--ne_panel=2", "--ne_vert=1", "--order=3", "--courant=4",
+                         "--end_time=40"],
     "acoustic_bdf2_c": ["--case=acoustic", "--integrator=bdf2", "--imex=1d", "--solver=direct",
                         "--equation_set=set2c", "--ne_panel=2", "--ne_vert=2", "--order=3",
                         "--courant=4", "--end_time=60"],

@@ -17,6 +17,9 @@ random velocity, and through the reference's public API:
        (build_column_jacobian, lam = 0.5 dt)
   X    ImplicitProblem.solve (direct) of the state, lam = 0.5 dt
   Q1,Q3  one and three ARK2 1D-IMEX direct steps at C_V = 5
+  X3g, X3b   the 3D-IMEX Schur solve (dim 3d) by GMRES and by BiCGstab +
+       PBNO (order 3), tol 1e-10, with their iteration counts; L3 the full
+       3D linear operator
   K1   one RK35 step at C_V = 0.5
 for each equation set; the mesh coordinates and DSS groups are stored so the
 tests can check the device path's mesh set-up first.  E-vector layout, fp64.
@@ -72,6 +75,14 @@ def run_case(N, ne_panel=2, ne_vert=2, seed=7):
             qs = imx.ark_imex_step(qs, dt, tab, prob, rhs)
             if k in (0, 2):
                 out[f"{sn}_Q{k + 1}"] = qs.copy()
+        # 3D-IMEX: the Schur pressure equation by GMRES and by BiCGstab + PBNO
+        for tag, spec in (("g", imx.SolverSpec(method="gmres", tol=1e-10)),
+                          ("b", imx.SolverSpec(method="bicgstab", tol=1e-10, precon_order=3))):
+            p3 = imx.ImplicitProblem(disc=disc, ref=ref, set_name=sn, form="schur", dim="3d", solver=spec)
+            p3.lam = 0.5 * dt
+            out[f"{sn}_X3{tag}"] = p3.solve(q)
+            out[f"{sn}_X3{tag}_it"] = np.array(p3.stats.iterations)
+        out[f"{sn}_L3"] = euler.linear_operator(q, ref, disc, sn)
         dte = 0.5 / cv
         out[f"{sn}_dte"] = np.array(dte)
         out[f"{sn}_K1"] = imx.rk35_step(q.copy(), dte, rhs)

@@ -40,8 +40,8 @@ def test_parse_config_defaults_overrides_and_errors(tmp_path):
 
 
 def test_unsupported_paths_raise():
-    # the sphere path runs the direct 1D-IMEX solve and RK35, not the Krylov solvers
-    for ov in (["--case=acoustic", "--integrator=ark2", "--imex=3d"], ["--integrator=ark2", "--form=standard"]):
+    # dG and the standard (5-variable) form are outside the device path
+    for ov in (["--disc=dg", "--equation_set=set2c"], ["--integrator=ark2", "--form=standard"]):
         with pytest.raises(NotImplementedError):
             driver._check_supported(driver.parse_config(None, ov))
 

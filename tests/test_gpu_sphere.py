@@ -132,3 +132,30 @@ def test_sphere_dss_and_derivatives():
     dv = disc.div_vc(mesh.vert * 1.0)
     assert np.isfinite(dv).all()
     del torch
+
+
+@pytest.mark.parametrize("N", [3, 4])
+@pytest.mark.parametrize("sn", ["set2nc", "set2c"])
+def test_sphere_imex3d(N, sn):
+    """3D-IMEX on the shell: the full linear operator, and the Schur pressure
+    equation by GMRES and by BiCGstab + PBNO (order 3), against the
+    reference's solutions and iteration counts."""
+    from paper_1702_04316_b200 import euler, imexcore as imx
+    d, mesh, ref, disc = _case(N)
+    q = d[f"{sn}_q0"]
+    dt = float(d[f"{sn}_dt"])
+    L3 = euler.linear_operator(q, ref, disc, sn)
+    G = d[f"{sn}_L3"]
+    buoy = np.abs(q[0] / ref.rho0).max() * ref.const.g
+    for f in range(5):
+        scale = np.abs(G[f]).max() + (buoy if f in (1, 2, 3) else 0.0)
+        assert np.abs(np.asarray(L3[f]) - G[f]).max() <= 1e-11 * scale, f
+    for tag, spec in (("g", imx.SolverSpec(method="gmres", tol=1e-10)),
+                      ("b", imx.SolverSpec(method="bicgstab", tol=1e-10, precon_order=3))):
+        p3 = imx.ImplicitProblem(disc=disc, ref=ref, set_name=sn, form="schur", dim="3d", solver=spec)
+        p3.lam = 0.5 * dt
+        X = p3.solve(q)
+        e = rel(X, d[f"{sn}_X3{tag}"])
+        print(sn, N, "X3" + tag, p3.stats.iterations, int(d[f"{sn}_X3{tag}_it"]), e)
+        assert abs(p3.stats.iterations - int(d[f"{sn}_X3{tag}_it"])) <= 1
+        assert e.max() < 1e-8, e
