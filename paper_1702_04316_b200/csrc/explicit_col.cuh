@@ -33,6 +33,9 @@
 
 #define EC_ZMAX 64
 #define EC_NMAX 4
+#ifndef HEVI_ECOL_TY
+#define HEVI_ECOL_TY 4   // tile rows in elements (2: two 128-thread CTAs per SM)
+#endif
 enum { C_RHO0 = 0, C_TH0, C_DRHO0, C_DTH0, C_CZ, C_IRHO0, C_G0, C_H0, C_PB, C_C0, C_IRT0, C_P0F,
        C_TH0C, C_ITH0, C_F0C, EC_NT };   // set2c: Theta0 = rho0 theta0, 1/Theta0, F0 = gamma P0f / Theta0
 
@@ -87,7 +90,7 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
 
 template <int N, int MODE>
 struct EC {
-    static constexpr int TX = 4, TY = 4;                      // elements per tile
+    static constexpr int TX = 4, TY = HEVI_ECOL_TY;           // elements per tile
     static constexpr int OX = TX * N, OY = TY * N;            // owned columns
     static constexpr int BLK = OX * OY;                       // one thread per column
     static constexpr int LX = OX + N + 1, LY = OY + N + 1;    // staged extent
@@ -104,7 +107,7 @@ struct EC {
     // from a double-buffered staging area: no per-store address arithmetic.
     // (Staging every output of every stage measured slower: 3.48 vs 3.27 ms.)
     static constexpr int NOUT = (MODE == M_S1) ? 10 : 0;
-    static constexpr int S = NAF ? 6 : (NOUT ? 7 : 8);        // ring slots
+    static constexpr int S = NAF ? 6 : (NOUT ? (TY == 4 ? 7 : 6) : 8);   // ring slots
     static constexpr int NXF = 6 * OY * TX, NYF = 6 * TY * OX;   // face partials per level
     static constexpr int DN = (N + 1) * (N + 1);
     static constexpr size_t SMEM =
@@ -251,7 +254,7 @@ __device__ __forceinline__ void ec_epilogue(const EArgs& a, const LvlTab& lt, lo
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(EC<N, MODE>::BLK, 1)
+__global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
     k_ecol(const EArgs a, const __grid_constant__ LvlTab lt, const __grid_constant__ CUtensorMap tmq,
            const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmA,
            const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmO0,

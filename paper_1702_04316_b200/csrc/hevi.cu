@@ -2427,7 +2427,7 @@ int hevi_stage_ex(hevi_plan* pl, int stage, double dt, const double* tab, double
 int hevi_stage_tiles(const hevi_plan* pl, int* n_interior, int* n_boundary) {
     if (!pl || !n_interior || !n_boundary) return fail("null argument");
     int tb[6];
-    tile_split(pl->g, 4, 4, tb);
+    tile_split(pl->g, 4, HEVI_ECOL_TY, tb);
     *n_interior = (tb[3] - tb[2]) * (tb[5] - tb[4]);
     *n_boundary = tb[0] * tb[1] - *n_interior;
     return HEVI_OK;
