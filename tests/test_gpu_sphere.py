@@ -159,3 +159,24 @@ def test_sphere_imex3d(N, sn):
         print(sn, N, "X3" + tag, p3.stats.iterations, int(d[f"{sn}_X3{tag}_it"]), e)
         assert abs(p3.stats.iterations - int(d[f"{sn}_X3{tag}_it"])) <= 1
         assert e.max() < 1e-8, e
+
+
+def test_sphere_hydrostatic_rest_state_stays_at_rest():
+    """The constant-theta hydrostatic background on the shell (grad theta0 = 0:
+    A^-1 is the identity, imexcore.py:203-206): the rest state is a discrete
+    equilibrium to round-off through R, L_V and ARK2 steps."""
+    from paper_1702_04316_b200 import specgrid as sg, euler, imexcore as imx
+    mesh = sg.build_cubed_sphere_mesh(2, 2, 6_371_000.0, 10_000.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    q = np.zeros((5,) + mesh.nshape)
+    R = euler.nonlinear_rhs(q, ref, disc, "set2nc")
+    L = euler.vertical_restriction(q, ref, disc, "set2nc")
+    assert np.abs(R).max() < 1e-9 and np.abs(L).max() < 1e-12
+    prob = imx.ImplicitProblem(disc=disc, ref=ref, set_name="set2nc", form="schur", dim="1d",
+                               solver=imx.SolverSpec(method="direct"))
+    rhs = euler.make_rhs(ref, disc, "set2nc")
+    qs = q
+    for _ in range(5):
+        qs = imx.ark_imex_step(qs, 30.0, imx.ark2_tableau(), prob, rhs)
+    assert np.abs(qs[1:4]).max() < 1e-7 and np.abs(qs[0]).max() < 1e-10
