@@ -188,6 +188,37 @@ def test_direct_solve_cost_flat_in_courant(box3):
     assert len(nbs) == 1
 
 
+def test_direct_solve_time_flat_in_courant():
+    """test_acceptance.py:442-468: the time of a direct solve is flat in the
+    Courant number (lam spans 100x): the spread of the median solve times
+    stays within 20 % (CUDA events, a 64x64x10-element box)."""
+    from paper_1702_04316_b200 import specgrid
+    mesh = specgrid.build_box_mesh_3d(64, 64, 10, 256_000.0, 256_000.0, 1000.0, 4)
+    ref = euler.hydrostatic_reference(mesh, 300.0)
+    disc = euler.build_discretization(mesh)
+    plan = disc.plan_for(ref)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    qe = plan.padded(0.01 * torch.rand((5, mesh.Z, mesh.Y, mesh.X), generator=g, device="cuda",
+                                       dtype=torch.float64))
+    out = plan.zeros()
+    med = []
+    for lam in (0.5, 5.0, 50.0):
+        plan.factor(lam)
+        for _ in range(3):
+            plan.solve(lam, qe, out)
+        ts = []
+        for _ in range(15):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            plan.solve(lam, qe, out)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        med.append(sorted(ts)[len(ts) // 2])
+    plan.check_flags()
+    assert max(med) <= 1.2 * min(med), med
+
+
 @pytest.mark.parametrize("integrator", ["ark2", "rk35"])
 def test_host_and_device_inputs_give_bitwise_equal_steps(box3, integrator):
     """Pinned host, device and numpy E-vectors through the fused entry points
