@@ -10,7 +10,7 @@ ops, stalls, lines = collections.Counter(), collections.Counter(), []
 for r in rows[2:]:
     try:
         n = int(r[ix["Instructions Executed"]]); s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
-    except (ValueError, KeyError):
+    except (ValueError, KeyError, IndexError):
         continue
     src = r[ix["Source"]].strip()
     m = re.match(r'(@!?U?P\w+\s+)?([A-Z][A-Z0-9_]*)', src)
