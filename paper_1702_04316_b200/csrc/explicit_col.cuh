@@ -88,6 +88,11 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
         : "memory");
 }
 
+template <int K>
+struct KI {
+    static constexpr int v = K;
+};
+
 template <int N, int MODE>
 struct EC {
     static constexpr int TX = 4, TY = HEVI_ECOL_TY;           // elements per tile
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
            const __grid_constant__ CUtensorMap tmO1, const __grid_constant__ CUtensorMap tmO2,
            const __grid_constant__ CUtensorMap tmO3) {
     using T = EC<N, MODE>;
-    constexpr int PL = T::PL, LXT = T::LXT, SS = T::SS, S = T::S, BLK = T::BLK;
+    constexpr int LXT = T::LXT, SS = T::SS, S = T::S, BLK = T::BLK;
     constexpr int OX = T::OX, OY = T::OY, TX = T::TX, TY = T::TY;
     constexpr bool NEED_L = (MODE == M_L || MODE == M_S1 || MODE == M_S2);
     constexpr bool NEED_R = (MODE != M_L);
@@ -401,54 +406,33 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
     faces(0, 0);
     __syncthreads();
 
-    int k = 0;
     unsigned fl = 0;   // flag bits of this thread's points (one atomic at the end)
-    for (int l = 0; l < Z; ++l) {
-        const bool top = (l == Z - 1);
-        if (k == 0 && !top) {
-            if (l > 0) {
-                // carries of the finished layer (row N of its element)
-#pragma unroll
-                for (int f = 0; f < 6; ++f) {
-                    double c = lt.dz[N * (N + 1)] * W[f][0];
-#pragma unroll
-                    for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], W[f][m], c);
-                    car[f] = c;
-                }
-                if (NEED_L) {
-                    double c = lt.dz[N * (N + 1)] * PLw[0];
-#pragma unroll
-                    for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], PLw[m], c);
-                    car[6] = c;
-                }
-            }
-#pragma unroll
-            for (int m = 1; m <= N; ++m) mbar_wait(&mbar[(l + m) % S], ((l + m) / S) & 1);
-#pragma unroll
-            for (int m = 0; m <= N; ++m) {
-                const double* sp = ring + ((l + m) % S) * SS + po;
-#pragma unroll
-                for (int f = 0; f < 6; ++f) W[f][m] = sp[T::foff(f)];
-                if (NEED_L) PLw[m] = lt.v[C_G0][l + m] * W[0][m] + lt.v[C_H0][l + m] * W[4][m];
-            }
-        }
+    // one level of the sweep; KK = the level's row in the window (static: the
+    // own point's values come from the window registers), N on the top level
+    auto level = [&](const int l, auto kc) {
+        constexpr int KK = decltype(kc)::v;
+        constexpr bool top = (KK == N);
+        // level parity (face-partial and staging double buffers): the layers
+        // start on levels l0 = 0 mod N (N even) and the top level Z-1 = nez N
+        constexpr int par = KK & 1;
+        static_assert(N % 2 == 0, "static level parity");
         const long long o = colo + (long long)l * zs;
         const double* slot = ring + (l % S) * SS;
-        const double* xfb = XFb + (l & 1) * T::NXF;
-        const double* yfb = YFb + (l & 1) * T::NYF;
+        const double* xfb = XFb + par * T::NXF;
+        const double* yfb = YFb + par * T::NYF;
         double dzr[N + 1];
 #pragma unroll
         for (int m = 0; m <= N; ++m) dzr[m] = lt.dzs[l][m];
         const double czf = lt.czf[l];
         const double rho0 = lt.v[C_RHO0][l];
 
-        // the point's own state (its window level is dynamic: read from the slot)
+        // the point's own state (window row KK)
         PtSt p;
-        p.r = slot[po];
-        p.u = slot[PL + po];
-        p.v = slot[2 * PL + po];
-        p.w = slot[3 * PL + po];
-        p.th = slot[4 * PL + po];
+        p.r = W[0][KK];
+        p.u = W[1][KK];
+        p.v = W[2][KK];
+        p.w = W[3][KK];
+        p.th = W[4][KK];
         p.rho = rho0 + p.r;
         p.rinv = NEED_R ? 1.0 / p.rho : 0.0;
         PtAcc c;
@@ -507,7 +491,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
                 // imexcore.py:398-403, 409-411: P, Quv by plain stores, A and F staged
                 const double dt = a.dt;
                 const double qv[5] = {p.r, p.u, p.v, p.w, p.th};
-                double* so = sOut + (l & 1) * (T::NOUT * OX * OY) + tid;
+                double* so = sOut + par * (T::NOUT * OX * OY) + tid;
                 double pr[5];
 #pragma unroll
                 for (int f = 0; f < 5; ++f) {
@@ -527,7 +511,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
                 ec_epilogue<MODE>(a, lt, o, l, p, Rv, Lv, Ai, Fi, bx, by, own, &fl);
             }
         }
-        if (l + 1 < Z) faces(l + 1, (l + 1) & 1);
+        if (l + 1 < Z) faces(l + 1, par ^ 1);
         if (T::NOUT) {
             // staged outputs visible to the async proxy; the store that read
             // the other staging buffer (level l-1) has finished reading it
@@ -536,7 +520,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
         }
         __syncthreads();
         if (T::NOUT && tid == 0) {
-            const double* so = sOut + (l & 1) * (T::NOUT * OX * OY);
+            const double* so = sOut + par * (T::NOUT * OX * OY);
             tma_store_4d(&tmO0, so, ax0, ay0, l, 0);                  // A
             tma_store_4d(&tmO1, so + 5 * OX * OY, ax0, ay0, l, 0);    // F
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -549,8 +533,41 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
             if (l + S < Z) issue(l + S);
             if (T::NAF && l + T::SAF < Z) issue_af(l + T::SAF);
         }
-        if (!top) k = (k + 1 == N) ? 0 : k + 1;
+    };
+    // element layers: the window (levels l0 .. l0+N) is loaded at the layer start
+    for (int l0 = 0; l0 + 1 < Z; l0 += N) {
+        const int l = l0;
+        if (l > 0) {
+            // carries of the finished layer (row N of its element)
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                double c = lt.dz[N * (N + 1)] * W[f][0];
+#pragma unroll
+                for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], W[f][m], c);
+                car[f] = c;
+            }
+            if (NEED_L) {
+                double c = lt.dz[N * (N + 1)] * PLw[0];
+#pragma unroll
+                for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], PLw[m], c);
+                car[6] = c;
+            }
+        }
+#pragma unroll
+        for (int m = 1; m <= N; ++m) mbar_wait(&mbar[(l + m) % S], ((l + m) / S) & 1);
+#pragma unroll
+        for (int m = 0; m <= N; ++m) {
+            const double* sp = ring + ((l + m) % S) * SS + po;
+#pragma unroll
+            for (int f = 0; f < 6; ++f) W[f][m] = sp[T::foff(f)];
+            if (NEED_L) PLw[m] = lt.v[C_G0][l + m] * W[0][m] + lt.v[C_H0][l + m] * W[4][m];
+        }
+        level(l0, KI<0>{});
+        level(l0 + 1, KI<1>{});
+        level(l0 + 2, KI<2>{});
+        level(l0 + 3, KI<3>{});
     }
+    level(Z - 1, KI<N>{});
     if (fl) atomicOr(a.flags, fl);
     if (T::NOUT && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
             const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmF) {
     using T = ECC<N, MODE>;
     constexpr int PL = T::PL, LXT = T::LXT, SS = T::SS, S = T::S, BLK = T::BLK;
-    constexpr int OX = T::OX, OY = T::OY, TX = T::TX, TY = T::TY, LX = T::LX, LY = T::LY;
+    constexpr int OX = T::OX, OY = T::OY, TX = T::TX, TY = T::TY, LY = T::LY;
     constexpr bool NEED_L = (MODE == M_S1 || MODE == M_S2);
     static_assert(N == 4, "x-line vector loads assume N = 4");
     static_assert(MODE == M_R || MODE == M_S1 || MODE == M_S2 || MODE == M_S3, "stage kernels and R");
@@ -276,37 +276,11 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
     faces(0, 0);
     __syncthreads();
 
-    int k = 0;
     unsigned fl = 0;
-    for (int l = 0; l < Z; ++l) {
-        const bool top = (l == Z - 1);
-        if (k == 0 && !top) {
-            if (l > 0) {
-#pragma unroll
-                for (int f = 0; f < 6; ++f) {
-                    double c = lt.dz[N * (N + 1)] * Wz[f][0];
-#pragma unroll
-                    for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], Wz[f][m], c);
-                    car[f] = c;
-                }
-            }
-#pragma unroll
-            for (int m = 1; m <= N; ++m) mbar_wait(&mbar[(l + m) % S], ((l + m) / S) & 1);
-#pragma unroll
-            for (int m = 0; m <= N; ++m) {
-                const double* sp = ring + ((l + m) % S) * SS + po;
-                const double r = sp[0], U = sp[PL], V = sp[2 * PL], W = sp[3 * PL], Th = sp[4 * PL];
-                const double rho = lt.v[C_RHO0][l + m] + r;
-                const double irho = 1.0 / rho;
-                const double theta = (lt.v[C_TH0C][l + m] + Th) * irho;
-                Wz[0][m] = W;
-                Wz[1][m] = (U * W) * irho;
-                Wz[2][m] = (V * W) * irho;
-                Wz[3][m] = (W * W) * irho + ecc_pprime(a, lt, l + m, rho, Th);
-                Wz[4][m] = theta * W;
-                Wz[5][m] = lt.v[C_F0C][l + m] * Th;
-            }
-        }
+    // one level of the sweep (KK: the level's row in the z-window, N on the top level)
+    auto level = [&](const int l, auto kc) {
+        constexpr int KK = decltype(kc)::v;   // -1: a rolled loop (row from the slot)
+        const bool top = (KK == N) || (KK < 0 && l == Z - 1);
         const double* slot = ring + (l % S) * SS;
         const double* pb = PB + (l & 1) * T::PBS;
         const double* xfb = XFb + (l & 1) * T::NXF;
@@ -315,7 +289,7 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
 #pragma unroll
         for (int m = 0; m <= N; ++m) dzr[m] = lt.dzs[l][m];
         const double czf = lt.czf[l];
-        const double r = slot[po], U = slot[PL + po], V = slot[2 * PL + po], W = slot[3 * PL + po],
+        const double r = slot[po], U = slot[PL + po], V = slot[2 * PL + po], W = KK >= 0 ? Wz[0][KK < 0 ? 0 : KK] : slot[3 * PL + po],
                      Th = slot[4 * PL + po];
         double gxq[5], gyq[5], gzq[6];
 #pragma unroll
@@ -389,7 +363,54 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
             if (l + S < Z) issue(l + S);
             if (T::NAF && l + T::SAF < Z) issue_af(l + T::SAF);
         }
-        if (!top) k = (k + 1 == N) ? 0 : k + 1;
+    };
+    // the z-window of the element layer starting at level l (levels l .. l+N)
+    auto zwin = [&](const int l) {
+        if (l > 0) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                double c = lt.dz[N * (N + 1)] * Wz[f][0];
+#pragma unroll
+                for (int m = 1; m <= N; ++m) c = fma(lt.dz[N * (N + 1) + m], Wz[f][m], c);
+                car[f] = c;
+            }
+        }
+#pragma unroll
+        for (int m = 1; m <= N; ++m) mbar_wait(&mbar[(l + m) % S], ((l + m) / S) & 1);
+#pragma unroll
+        for (int m = 0; m <= N; ++m) {
+            const double* sp = ring + ((l + m) % S) * SS + po;
+            const double r = sp[0], U = sp[PL], V = sp[2 * PL], W = sp[3 * PL], Th = sp[4 * PL];
+            const double rho = lt.v[C_RHO0][l + m] + r;
+            const double irho = 1.0 / rho;
+            const double theta = (lt.v[C_TH0C][l + m] + Th) * irho;
+            Wz[0][m] = W;
+            Wz[1][m] = (U * W) * irho;
+            Wz[2][m] = (V * W) * irho;
+            Wz[3][m] = (W * W) * irho + ecc_pprime(a, lt, l + m, rho, Th);
+            Wz[4][m] = theta * W;
+            Wz[5][m] = lt.v[C_F0C][l + m] * Th;
+        }
+    };
+    if (MODE == M_S1) {
+        // rolled (unrolled, stage 0 rises from 228 to 240 registers and slows by 3 %)
+        int k = 0;
+        for (int l = 0; l < Z; ++l) {
+            const bool last = (l == Z - 1);
+            if (k == 0 && !last) zwin(l);
+            level(l, KI<-1>{});
+            if (!last) k = (k + 1 == N) ? 0 : k + 1;
+        }
+    } else {
+        // element layers, unrolled: the own point's W is window row KK
+        for (int l0 = 0; l0 + 1 < Z; l0 += N) {
+            zwin(l0);
+            level(l0, KI<0>{});
+            level(l0 + 1, KI<1>{});
+            level(l0 + 2, KI<2>{});
+            level(l0 + 3, KI<3>{});
+        }
+        level(Z - 1, KI<N>{});
     }
     if (fl) atomicOr(a.flags, fl);
 }

@@ -160,6 +160,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 #define HEVI_PP_SHORT 1
 #endif
 
+// the rare |delta| > 1/8 branch of P', out of line: one copy per kernel
+// instead of one per inlined call site (the column kernels' code size and
+// register budget)
+__device__ __noinline__ double pprime_pow(double rho, double theta, double P0f, double P0, double R,
+                                          double gamma) {
+    return P0 * pow(rho * R * theta / P0, gamma) - P0f;
+}
+
 // P' at one point; rho0/theta0/Pb/c0/irt0 of its level
 __device__ __forceinline__ double pprime(double r, double th, double rho0, double th0, double Pb,
                                          double c0, double irt0, double P0f, const double* bc,
@@ -178,8 +186,7 @@ __device__ __forceinline__ double pprime(double r, double th, double rho0, doubl
         for (int k = 13; k >= 0; --k) s = fma(s, delta, bc[k]);
         return fma(Pb, s * delta, c0);
     }
-    const double rho = rho0 + r, theta = th0 + th;
-    return ph.P0 * pow(rho * ph.R * theta / ph.P0, ph.gamma) - P0f;
+    return pprime_pow(rho0 + r, th0 + th, P0f, ph.P0, ph.R, ph.gamma);
 }
 
 template <int N, int NY, int K>

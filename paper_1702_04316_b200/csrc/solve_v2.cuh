@@ -33,13 +33,6 @@ struct S2Args {
     double bc[16];
 };
 
-// the rare |delta| > 1/8 branch of pprime, out of line (keeps the column
-// kernel's register budget)
-__device__ __noinline__ double pprime_pow(double rho, double theta, double P0f, double P0, double R,
-                                          double gamma) {
-    return P0 * pow(rho * R * theta / P0, gamma) - P0f;
-}
-
 // P' of a solved point: the explicit kernel's pprime (explicit_v2.cuh) on the
 // same inputs, written once here instead of per staged point downstream
 // PT: the level's [rho0 | theta0 | 1/(rho0 theta0) | Pb | Pb - P0f | P0f]
