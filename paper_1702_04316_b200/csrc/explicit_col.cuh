@@ -356,7 +356,22 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
     const long long zs = (long long)g.lY * g.px;
     const double gr = a.ph.g;
 
-    // element-face partials (row N of the left / lower element) of level l
+    // element-face partials (row N of the left / lower element) of level l;
+    // a thread's items and their slot offsets are the same on every level
+    static_assert(T::NXF + T::NYF <= 3 * BLK, "faces: three items per thread");
+    int fo[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int i = tid + r * BLK;
+        if (i < T::NXF) {
+            const int f = i / (OY * TX), rem = i % (OY * TX);
+            fo[r] = T::foff(f) + (rem / TX + N) * LXT + (rem % TX) * N;
+        } else {
+            const int ii = i - T::NXF;
+            const int f = ii / (TY * OX), rem = ii % (TY * OX);
+            fo[r] = T::foff(f) + (rem / OX) * N * LXT + rem % OX + N;
+        }
+    }
     auto faces = [&](int l, int buf) {
         if (!NEED_R) return;
         const double* slot = ring + (l % S) * SS;
@@ -366,9 +381,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
         for (int r = 0; r < 3; ++r) {
             int i = tid + r * BLK;
             if (i < T::NXF) {
-                const int f = i / (OY * TX), rem = i % (OY * TX);
-                const int yy = rem / TX, j = rem % TX;
-                const double* s = slot + T::foff(f) + (yy + N) * LXT + j * N;
+                const double* s = slot + fo[r];
                 const double2 v01 = *reinterpret_cast<const double2*>(s);
                 const double2 v23 = *reinterpret_cast<const double2*>(s + 2);
                 double d = lt.dx[N * (N + 1) + 0] * v01.x;
@@ -379,9 +392,7 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
                 xf[i] = d;
             } else if (i < T::NXF + T::NYF) {
                 i -= T::NXF;
-                const int f = i / (TY * OX), rem = i % (TY * OX);
-                const int j = rem / OX, xx = rem % OX;
-                const double* s = slot + T::foff(f) + (j * N) * LXT + xx + N;
+                const double* s = slot + fo[r];
                 double d = lt.dy[N * (N + 1)] * s[0];
 #pragma unroll
                 for (int m = 1; m <= N; ++m) d = fma(lt.dy[N * (N + 1) + m], s[m * LXT], d);
