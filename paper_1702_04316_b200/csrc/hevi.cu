@@ -1268,6 +1268,7 @@ struct hevi_plan {
     unsigned* h_flags = nullptr;
     std::map<long long, Factor> factors;
     double bc[16];
+    double hDz[81];   // host copy of the vertical D matrix (the column kernels' parameter bank)
     int eqset = 0;   // 0: set2nc, 1: set2c
     int force_pivoted = 0;   // HEVI_OPT_FORCE_PIVOTED (tests of the fallback path)
     // the column solve of stage s wrote P' of its output into the P buffer's
@@ -1876,6 +1877,7 @@ int launch_s2(const hevi_plan* pl, const Factor* f, const SArgs& a1, cudaStream_
     a.LU2 = f->LU2;
     a.rU = f->rU;
     a.Dz = pl->Dz;
+    memcpy(a.Dzc, pl->hDz, sizeof(a.Dzc));
     a.ainv_identity = pl->ainv_identity;
     a.lam = f->lam;
     a.P = a1.P;
@@ -2072,6 +2074,7 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
     h.insert(h.end(), rd->Dx, rd->Dx + nd);
     h.insert(h.end(), rd->Dy, rd->Dy + ndy);
     h.insert(h.end(), rd->Dz, rd->Dz + nd);
+    memcpy(pl->hDz, rd->Dz, sizeof(double) * nd);
     // EOS reference point per level: Pb = EOS(rho0, theta0), c0 = Pb - P0f, 1/(rho0 theta0)
     h.insert(h.end(), rd->Pb, rd->Pb + Z);
     for (int k = 0; k < Z; ++k) h.push_back(rd->Pb[k] - rd->P0f[k]);

@@ -31,6 +31,7 @@ struct S2Args {
     const double* rec;     // k_solve2's per-level records (k_s2rec)
     Lev lv;
     double bc[16];
+    double Dzc[81];        // the D matrix in the parameter bank (k_solve2: static indices)
 };
 
 // P' of a solved point: the explicit kernel's pprime (explicit_v2.cuh) on the
@@ -119,7 +120,11 @@ __host__ __device__ constexpr size_t s2_smem_bytes(int M, int T) {
 #endif
 
 template <int N, bool SC>   // SC: conservative set set2c
-__global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
+// (128, 1): ptxas takes 164 registers (12 warps per SM) -- faster than the
+// 128-register, 16-warp schedule of __launch_bounds__(128) / (128, 4): the
+// column chains gain more from registers than from resident warps
+// (0.2975 -> 0.288 ms per solve)
+__global__ void __launch_bounds__(128, 1) k_solve2(const S2Args a) {
     using R = S2Rec<N>;
     constexpr int RS = R::RS;
     extern __shared__ __align__(16) double sm2[];
@@ -128,14 +133,19 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     const int T = blockDim.x;
     const int tid = threadIdx.x;
     double* rec = sm2;                        // M * RS
-    double* sD = rec + (size_t)M * RS;        // (N+1)^2
+    double* sD = rec + (size_t)M * RS;        // (N+1)^2 (set2c)
     double* Y = sD + (N + 1) * (N + 1);       // M * T
+    // the vertical D matrix: set2nc reads the parameter bank (static indices,
+    // no shared loads: -1.4 % per solve); set2c keeps shared memory (the
+    // parameter-bank form measured 8 % slower there)
+#define DZC(i) (SC ? sD[i] : a.Dzc[i])
     {
         const double2* src = reinterpret_cast<const double2*>(a.rec);
         double2* dst = reinterpret_cast<double2*>(rec);
         for (int i = tid; i < M * RS / 2; i += T) dst[i] = src[i];
     }
-    for (int i = tid; i < (N + 1) * (N + 1); i += T) sD[i] = a.Dz[i];
+    if (SC)
+        for (int i = tid; i < (N + 1) * (N + 1); i += T) sD[i] = a.Dz[i];
     __syncthreads();
 
     const int NYo = g.slab ? 1 : N;
@@ -232,7 +242,7 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
             const double* rk = r0 + l * RS;
             double d = 0.0;
 #pragma unroll
-            for (int m = 0; m <= N; ++m) d = fma(sD[l * (N + 1) + m], uaw[m], d);
+            for (int m = 0; m <= N; ++m) d = fma(DZC(l * (N + 1) + m), uaw[m], d);
             if (l == 0 && e > 0) d += carry;
             const double dua = TBk(rk, V_CZ) * d;
             // imexcore._helmholtz_flux (imexcore.py:263-268)
@@ -248,7 +258,7 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
         // row N of this element: the lower half of the next face derivative
         double cr = 0.0;
 #pragma unroll
-        for (int m = 0; m <= N; ++m) cr = fma(sD[N * (N + 1) + m], uaw[m], cr);
+        for (int m = 0; m <= N; ++m) cr = fma(DZC(N * (N + 1) + m), uaw[m], cr);
         carry = cr;
         if (e + 1 < nez) {
 #pragma unroll
@@ -353,11 +363,11 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
             for (int l = 1; l <= N; ++l, o += ls) {
                 double d = 0.0;
 #pragma unroll
-                for (int m = 0; m <= N; ++m) d = fma(sD[l * (N + 1) + m], xw[m], d);
+                for (int m = 0; m <= N; ++m) d = fma(DZC(l * (N + 1) + m), xw[m], d);
                 if (l == N && e + 1 < nez) {
                     double d2 = 0.0;
 #pragma unroll
-                    for (int m = 0; m <= N; ++m) d2 = fma(sD[m], xw[N + m], d2);
+                    for (int m = 0; m <= N; ++m) d2 = fma(DZC(m), xw[N + m], d2);
                     d += d2;
                 }
                 extract(r0 + l * RS, k0 + l, o, xw[l], d, ro[l - 1], we[l - 1], te[l - 1]);
@@ -371,11 +381,12 @@ __global__ void __launch_bounds__(128) k_solve2(const S2Args a) {
     {   // bottom level: row 0 of element 0, boundary
         double d = 0.0;
 #pragma unroll
-        for (int m = 0; m <= N; ++m) d = fma(sD[m], xw[m], d);
+        for (int m = 0; m <= N; ++m) d = fma(DZC(m), xw[m], d);
         extract(rec, 0, 0, xw[0], d, SC ? Po[0] : 0.0, Po3[0], Po4[0]);
     }
     }   // column blocks
 #undef TBk
+#undef DZC
 }
 
 // ---------------------------------------------------------------------------
