@@ -32,6 +32,16 @@
 #pragma once
 
 #define EC_ZMAX 64
+// domain-end kernel as a programmatic dependent launch of the sweep (else
+// forked onto the plan's side stream): measured per equation set -- set2c
+// 4.35 -> 4.15 ms per step with it; set2nc within 0.3 % at one GPU and 1-2 %
+// slower at the x-end ranks of 2/4/8-GPU windows, so set2nc forks
+#ifndef HEVI_EDGE_PDL_NC
+#define HEVI_EDGE_PDL_NC 0
+#endif
+#ifndef HEVI_EDGE_PDL_C
+#define HEVI_EDGE_PDL_C 1
+#endif
 #define EC_NMAX 4
 #ifndef HEVI_ECOL_TY
 #define HEVI_ECOL_TY 4   // tile rows in elements (2: two 128-thread CTAs per SM)
@@ -293,6 +303,18 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
     const bool own = gx < g.ex_e * N && gy < g.ey_e * N;
     const int tx0 = (ex0 - 1) * N - g.x0, ty0 = (ey0 - 1) * N - g.y0;
 
+    // the domain-end kernel launched after this one (programmatic dependent
+    // launch) may start once every tile of this grid is resident: it then
+    // fills the SMs the last wave leaves idle instead of delaying that wave
+    if (HEVI_EDGE_PDL_NC) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef HEVI_EDGE_TIMING
+    if (tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(a.dbg + 0, ~0ull - t);
+        atomicMax(a.dbg + 1, t);
+    }
+#endif
     if (tid == 0) {
         for (int s = 0; s < S + T::SAF; ++s) mbar_init(&mbar[s], 1);
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmq) : "memory");
@@ -581,6 +603,20 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
     level(Z - 1, KI<N>{});
     if (fl) atomicOr(a.flags, fl);
     if (T::NOUT && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifdef HEVI_EDGE_TIMING
+    if (tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(a.dbg + 2, t);
+    }
+#endif
+}
+
+// end of a domain-end kernel launched as a programmatic dependent of the
+// sweep: the grid completes only after the sweep has (the stream work that
+// follows reads both); a no-op for an ordinary launch
+__device__ __forceinline__ void ec_edge_done() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // the domain-end planes x = X-1 / y = Y-1 inside the rank's ownership: one
@@ -603,6 +639,13 @@ __global__ void __launch_bounds__(128) k_ecol_edge(const EArgs a, const __grid_c
     // points: nxc column points (x = X-1, y = ylo ..), then nyr row points (y = Y-1, x = xlo ..), per level
     const long long per = (long long)nxc + nyr;
     const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+#ifdef HEVI_EDGE_TIMING
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(a.dbg + 3, ~0ull - t);
+    }
+#endif
     if (id >= per * G.Z) return;
     const int gz = (int)(id / per);
     const int cc = (int)(id % per);
@@ -709,4 +752,12 @@ __global__ void __launch_bounds__(128) k_ecol_edge(const EArgs a, const __grid_c
         if (MODE == M_S2 || MODE == M_S3) Fi[f] = a.F[o + f * fs];
     }
     ec_epilogue<MODE>(a, lt, o, gz, p, Rv, Lv, Ai, Fi, bx, by);
+#ifdef HEVI_EDGE_TIMING
+    {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(a.dbg + 4, t);
+    }
+#endif
+    ec_edge_done();
 }

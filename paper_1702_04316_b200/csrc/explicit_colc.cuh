@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(ECC<N, MODE>::BLK, 1)
     const bool own = gx < g.ex_e * N && gy < g.ey_e * N;
     const int tx0 = (ex0 - 1) * N - g.x0, ty0 = (ey0 - 1) * N - g.y0;
 
+    if (HEVI_EDGE_PDL_C) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // see k_ecol
     if (tid == 0) {
         for (int s = 0; s < S + T::SAF; ++s) mbar_init(&mbar[s], 1);
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmq) : "memory");
@@ -543,4 +544,5 @@ __global__ void __launch_bounds__(128) k_ecolc_edge(const EArgs a, const __grid_
     p.w = W;
     p.th = Th;
     ec_epilogue<MODE>(a, lt, o, gz, p, Rv, Lv, Ai, Fi, bx, by);
+    ec_edge_done();
 }

@@ -1603,6 +1603,27 @@ int dispatch_c(const hevi_plan* pl, const EArgs& a, cudaStream_t st) {
     return fail("set2c: unsupported polynomial order for the device path");
 }
 
+#ifndef HEVI_SKIP_EDGE
+#define HEVI_SKIP_EDGE 0   // timing experiments only: no domain-end kernel (wrong results)
+#endif
+// a launch that may overlap the stream's previous kernel once that kernel's
+// CTAs have all executed griddepcontrol.launch_dependents
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned blocks, unsigned threads, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---- explicit_col dispatch (3D box, N = 4, set2nc, stage kernels) --------
 // cudaFuncSetAttribute once per (kernel, device)
 
@@ -1689,14 +1710,20 @@ int launch_col(const hevi_plan* pl, const EArgs& a0, cudaStream_t st) {
     const bool partial_end = ((g.ex_e == g.nex) && (g.ex_e - g.ex_b) % T::TX != 0) ||
                              ((g.ey_e == g.ney) && (g.ey_e - g.ey_b) % T::TY != 0);
     const dim3 grid = tile_grid(a, g, T::TX, T::TY);
-    const bool edge = npt > 0 && a.tmode != 1;   // the interior subset has no domain-end plane
-    const bool fork = edge && pl->side != nullptr && !(T::NOUT && partial_end);
+    const bool edge = !HEVI_SKIP_EDGE && npt > 0 && a.tmode != 1;   // the interior subset has no domain-end plane
+    // the domain-end kernel as a programmatic dependent launch of the sweep
+    // (starts once every sweep tile is resident; completes after the sweep)
+    const bool pdl = HEVI_EDGE_PDL_NC && edge && grid.x && grid.y && !(T::NOUT && partial_end);
+    const bool fork = !pdl && edge && pl->side != nullptr && !(T::NOUT && partial_end);
     if (fork) CK(cudaEventRecord(pl->ev_fork, st));
     if (grid.x && grid.y) {
         kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tp, tA, tF, o0, o1, o2, o3);
         CK(cudaGetLastError());
     }
-    if (edge) {
+    if (pdl) {
+        CK(launch_pdl(k_ecol_edge<N, MODE>, (unsigned)((npt + 127) / 128), 128, st, a, pl->lt, nxc, nyr,
+                      g.ex_b * N, g.ey_b * N));
+    } else if (edge) {
         // launched after the sweep: its blocks are dispatched as the sweep's last CTAs retire
         cudaStream_t es = fork ? pl->side : st;
         if (fork) CK(cudaStreamWaitEvent(es, pl->ev_fork, 0));
@@ -1733,13 +1760,17 @@ int launch_colc(const hevi_plan* pl, const EArgs& a0, cudaStream_t st) {
     const long long npt = (long long)(nxc + nyr) * g.Z;
     const dim3 grid = tile_grid(a, g, T::TX, T::TY);
     const bool edge = npt > 0 && a.tmode != 1;
-    const bool fork = edge && pl->side != nullptr;
+    const bool pdl = HEVI_EDGE_PDL_C && edge && grid.x && grid.y;
+    const bool fork = !pdl && edge && pl->side != nullptr;
     if (fork) CK(cudaEventRecord(pl->ev_fork, st));
     if (grid.x && grid.y) {
         kern<<<grid, T::BLK, T::SMEM, st>>>(a, pl->lt, tq, tA, tF);
         CK(cudaGetLastError());
     }
-    if (edge) {
+    if (pdl) {
+        CK(launch_pdl(k_ecolc_edge<N, MODE>, (unsigned)((npt + 127) / 128), 128, st, a, pl->lt, nxc, nyr,
+                      g.ex_b * N, g.ey_b * N));
+    } else if (edge) {
         cudaStream_t es = fork ? pl->side : st;
         if (fork) CK(cudaStreamWaitEvent(es, pl->ev_fork, 0));
         k_ecolc_edge<N, MODE><<<(unsigned)((npt + 127) / 128), 128, 0, es>>>(a, pl->lt, nxc, nyr, g.ex_b * N,
@@ -2017,7 +2048,7 @@ extern "C" {
 
 const char* hevi_last_error(void) { return g_err.c_str(); }
 
-#ifdef HEVI_PHASE_TIMING
+#if defined(HEVI_PHASE_TIMING) || defined(HEVI_EDGE_TIMING)
 // debug builds only: per-phase clock64 sums of the explicit kernel, reset after read
 int hevi_debug_phase(hevi_plan* pl, unsigned long long* out8) {
     CK(cudaDeviceSynchronize());
@@ -2101,7 +2132,7 @@ int hevi_plan_create(hevi_plan** out, const hevi_grid_desc* gd, const hevi_ref_d
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming);
     }
-#ifdef HEVI_PHASE_TIMING
+#if defined(HEVI_PHASE_TIMING) || defined(HEVI_EDGE_TIMING)
     if (e == cudaSuccess) e = cudaMalloc(&pl->d_dbg, 8 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(pl->d_dbg, 0, 8 * sizeof(unsigned long long));
 #endif
