@@ -146,6 +146,23 @@ def test_stepper_graph_replay_matches_eager(setup):
     assert torch.equal(st.state(lattice=True), want)
 
 
+def test_stepper_graph_replay_matches_eager_set2c(setup):
+    """set2c launches its domain-end kernel as a programmatic dependent of
+    the sweep: captured in a CUDA graph and replayed it gives the eager bits."""
+    mesh, ref, disc, _, _ = setup
+    q0 = cases.bubble_lattice(mesh, ref, 0.5, (16_000.0, 12_000.0, 150.0), (6000.0, 6000.0, 100.0),
+                              set_name="set2c")
+    dt = cases.dt_for_courant(mesh, ref, q0, 15.0, "set2c")
+    eager = HeviStepper(disc, ref, dt, set_name="set2c")
+    eager.set_state(q0, lattice=True)
+    eager.step(3)
+    st = HeviStepper(disc, ref, dt, set_name="set2c")
+    st.set_state(q0, lattice=True)
+    st.capture()          # records (and runs) one step
+    st.step(2)
+    assert torch.equal(st.state(lattice=True), eager.state(lattice=True))
+
+
 def test_resident_stepper_matches_drop_in_step(setup):
     mesh, ref, disc, q0, dt = setup
     plan = disc.plan_for(ref)
