@@ -120,11 +120,13 @@ __host__ __device__ constexpr size_t s2_smem_bytes(int M, int T) {
 #endif
 
 template <int N, bool SC>   // SC: conservative set set2c
-// (128, 1): ptxas takes 164 registers (12 warps per SM) -- faster than the
-// 128-register, 16-warp schedule of __launch_bounds__(128) / (128, 4): the
-// column chains gain more from registers than from resident warps
-// (0.2975 -> 0.288 ms per solve)
-__global__ void __launch_bounds__(128, 1) k_solve2(const S2Args a) {
+// (128, 3): at most 168 registers, 12 warps per SM (3 per scheduler: the
+// register file is split 16 K per sub-partition) -- faster than the
+// 128-register, 16-warp schedule of __launch_bounds__(128) (0.2975 -> 0.288
+// ms per solve) and, with the backward lines loaded one element ahead, than
+// the 184-register, 8-warp schedule that look-ahead takes unbounded (0.274
+// vs 0.325 ms)
+__global__ void __launch_bounds__(128, 3) k_solve2(const S2Args a) {
     using R = S2Rec<N>;
     constexpr int RS = R::RS;
     extern __shared__ __align__(16) double sm2[];
@@ -324,6 +326,19 @@ __global__ void __launch_bounds__(128, 1) k_solve2(const S2Args a) {
         }
     };
 
+    // the extraction's predictor lines of an element, loaded one element
+    // ahead (in flight during the element above's substitution)
+    double wn[N], tn[N], rn[N];
+    auto load_bwd = [&](int e) {
+        int o = (e * N + 1) * ls;
+#pragma unroll
+        for (int l = 1; l <= N; ++l, o += ls) {
+            wn[l - 1] = Po3[o];
+            tn[l - 1] = Po4[o];
+            rn[l - 1] = SC ? Po[o] : 0.0;
+        }
+    };
+    load_bwd(nez - 1);
     for (int e = nez - 1; e >= 0; --e) {
         const int k0 = e * N;
         const double* r0 = rec + k0 * RS;
@@ -339,15 +354,13 @@ __global__ void __launch_bounds__(128, 1) k_solve2(const S2Args a) {
             }
         }
         double we[N], te[N], ro[N];
-        {
-            int o = o1;
 #pragma unroll
-            for (int l = 1; l <= N; ++l, o += ls) {
-                we[l - 1] = Po3[o];
-                te[l - 1] = Po4[o];
-                ro[l - 1] = SC ? Po[o] : 0.0;
-            }
+        for (int l = 0; l < N; ++l) {
+            we[l] = wn[l];
+            te[l] = tn[l];
+            ro[l] = rn[l];
         }
+        if (e > 0) load_bwd(e - 1);
 #pragma unroll
         for (int l = N - 1; l >= 0; --l) {
             const double* rk = r0 + l * RS;
