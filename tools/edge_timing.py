@@ -1,6 +1,10 @@
 """Timeline of one explicit stage at an 8-GPU rank window (x-end rank 3):
-sweep CTA start/end and domain-end kernel start/end from %globaltimer
-(HEVI_EDGE_TIMING build via HEVI_LIB).  GPU only."""
+sweep CTA start/end and domain-end kernel start/end from %globaltimer.
+GPU only; needs a timing build:
+
+    bash tools/dev_build.sh et -DHEVI_EDGE_TIMING -DHEVI_EDGE_PDL_NC=1
+    HEVI_LIB=paper_1702_04316_b200/_lib/libhevi_et.so python tools/edge_timing.py [rank]
+"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
