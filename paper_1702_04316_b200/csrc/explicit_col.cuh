@@ -608,6 +608,9 @@ __global__ void __launch_bounds__(EC<N, MODE>::BLK, 4 / HEVI_ECOL_TY)
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         atomicMax(a.dbg + 2, t);
+        // the end of the tiles before the last partial wave (148 SMs; tools/tail_timing.py)
+        const unsigned nb = gridDim.x * gridDim.y, b = blockIdx.x + blockIdx.y * gridDim.x;
+        if (b < nb - nb % 148u) atomicMax(a.dbg + 5, t);
     }
 #endif
 }

@@ -1,6 +1,11 @@
-"""Wave tail of one explicit stage at config 5 on one B200 (HEVI_EDGE_TIMING
-build via HEVI_LIB): when the tiles before the last partial wave end vs the
-last tile, from %globaltimer.  GPU only."""
+"""Wave tail of one explicit stage at config 5 (a rank window of an N-GPU
+decomposition, timed alone on one B200): when the tiles before the last
+partial wave end vs the last tile, from %globaltimer.  GPU only; needs a
+timing build:
+
+    bash tools/dev_build.sh tt -DHEVI_EDGE_TIMING
+    HEVI_LIB=paper_1702_04316_b200/_lib/libhevi_tt.so python tools/tail_timing.py [world] [rank]
+"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
